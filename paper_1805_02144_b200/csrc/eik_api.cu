@@ -1,0 +1,1171 @@
+// eik_api.cu -- kernels and the C ABI (include/eik.h) of libeik.so.
+//
+// Host side owns: the ELL stencil built from the reference's CSR operators,
+// device buffers, one CUDA stream per context, cooperative launches and the
+// CUDA graph of a whole integrator step.  No compute runs on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "eik_dev.cuh"
+
+using namespace eik;
+
+// ====================================================================== errors
+static thread_local std::string g_err;
+static eik_status fail(eik_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(EIK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ====================================================================== kernels
+
+__device__ __forceinline__ void smem_init(Smem& sm) {
+  if (threadIdx.x == 0) sm.par = 0;
+  __syncthreads();
+}
+
+// (u_x; u_y; u_z; h) SoA  <->  per-cell double4
+__global__ void k_soa_to_cell(const double* __restrict__ s, double4* d, int64_t N) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = make_double4(s[i], s[N + i], s[2 * N + i], s[3 * N + i]);
+}
+__global__ void k_cell_to_soa(const double4* __restrict__ d, double* s, int64_t N) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double4 v = d[i];
+    s[i] = v.x;
+    s[N + i] = v.y;
+    s[2 * N + i] = v.z;
+    s[3 * N + i] = v.w;
+  }
+}
+
+struct SweArgs {
+  SweOp S;
+  EngineWork Wk;
+  // step buffers
+  double4 *u, *uprev, *fn, *v1, *va, *vb, *d2, *Ub, *W[5];
+  // API buffers
+  double4 *x, *out;
+  double dt, tol;
+  double c09cube;      // 0.9 ** 3 as CPython computes it
+  int scheme;
+  int* status;         // device status word
+  double* nnz_out;
+  double* dbg;         // optional per-row output (nnz per cell)
+  EngineTask task;     // engine-level API
+};
+
+// F(w) (+ eta at w when `lin` is w); optional out_v = dt * F.
+// returns a status uniform over the grid.
+__device__ int phase_rhs(cg::grid_group& grid, Smem& sm, const SweOp& S,
+                         const double4* w, double4* out_f, double4* out_v,
+                         double dt, bool write_eta, double* part) {
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  SrcPtr src{w};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) S.lapA[i] = swe_lap_cell(S, src, i);
+  grid.sync();
+  double r[1] = {0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
+    double eta;
+    const double4 F = swe_rhs_cell(S, src, S.lapA, i, &eta);
+    if (write_eta) {
+      const double4 q = S.nf[i];
+      S.ne[i] = make_double4(q.x, q.y, q.z, eta);
+    }
+    if (out_f) out_f[i] = F;
+    if (out_v) out_v[i] = dt * F;
+    r[0] += nf4(F) + nf4(w[i]);
+  }
+  grid_reduce<1>(grid, sm, r, part);
+  return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
+}
+
+// d = (F(U) - f_n) - J (U - u_n)   (integrators.py:101-102), epilogue(i, d)
+template <class Epi>
+__device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
+                         const double4* U, const double4* fn, Epi epi,
+                         double* part) {
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  SrcPtr su{U};
+  SrcDiff sx{U, S.lin};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
+    S.lapA[i] = swe_lap_cell(S, su, i);
+    S.lapB[i] = swe_lap_cell(S, sx, i);
+  }
+  grid.sync();
+  double r[1] = {0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
+    double eta;
+    const double4 F = swe_rhs_cell(S, su, S.lapA, i, &eta);
+    const double4 Jx = swe_jv_cell(S, sx, S.lapB, i);
+    const double4 d = (F - fn[i]) - Jx;
+    epi(i, d);
+    r[0] += nf4(F) + nf4(U[i]);
+  }
+  grid_reduce<1>(grid, sm, r, part);
+  return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
+}
+
+// n_A = nnz of the assembled J = (J_v + J_r) + J_m with scipy's zero-dropping
+// (swe.py:175-223).  Products and sums use _rn
+// intrinsics so exact zeros come out exactly as in numpy.
+__device__ double phase_count_nnz(cg::grid_group& grid, Smem& sm, const SweOp& S,
+                                  double* part, double* per_row = nullptr) {
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  double r[1] = {0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
+    const double4 Ui = S.lin[i];
+    const int cn = __ldg(S.cnt + i);
+    // eta exactly as numpy: ((Vx@ux + Vy@uy) + Vz@uz) + f, each csr_matvec
+    // a sequential sum in column order, no FMA
+    double sv[3] = {0.0, 0.0, 0.0};
+    for (int s = 0; s < cn; ++s) {
+      const double4 Uj = S.lin[S.nb(s, i)];
+      sv[0] = __dadd_rn(sv[0], __dmul_rn(S.c(s, OP_VX, i), Uj.x));
+      sv[1] = __dadd_rn(sv[1], __dmul_rn(S.c(s, OP_VY, i), Uj.y));
+      sv[2] = __dadd_rn(sv[2], __dmul_rn(S.c(s, OP_VZ, i), Uj.z));
+    }
+    const double4 nfi = S.nf[i];
+    const double4 q = make_double4(nfi.x, nfi.y, nfi.z,
+                                   __dadd_rn(__dadd_rn(__dadd_rn(sv[0], sv[1]), sv[2]), nfi.w));
+    const double P[3] = {__dsub_rn(__dmul_rn(q.y, Ui.z), __dmul_rn(q.z, Ui.y)),
+                         __dsub_rn(__dmul_rn(q.z, Ui.x), __dmul_rn(q.x, Ui.z)),
+                         __dsub_rn(__dmul_rn(q.x, Ui.y), __dmul_rn(q.y, Ui.x))};
+    const double ex = __dmul_rn(q.w, q.x), ey = __dmul_rn(q.w, q.y),
+                 ez = __dmul_rn(q.w, q.z);
+    // Jr off-diagonal blocks (a,b): xy +ez, xz -ey, yx -ez, yz +ex, zx +ey, zy -ex
+    const double rot[3][3] = {{0.0, ez, -ey}, {-ez, 0.0, ex}, {ey, -ex, 0.0}};
+    double c = 4.0 * (double)__ldg(S.dfx + i);
+    for (int s = 0; s < cn; ++s) {
+      const int64_t j = S.nb(s, i);
+      const double4 Uj = S.lin[j];
+      const double uj[3] = {Uj.x, Uj.y, Uj.z};
+      const double df = __ldg(S.df1 + (int64_t)s * S.N + i);
+      double G[3], D[3], V[3];
+      for (int k = 0; k < 3; ++k) {
+        G[k] = S.c(s, OP_GX + k, i);
+        D[k] = S.c(s, OP_DX + k, i);
+        V[k] = S.c(s, OP_VX + k, i);
+      }
+      for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) {
+          const double jv = -__dmul_rn(P[a], V[b]);
+          const double jr = (a == b) ? df : (j == i ? rot[a][b] : 0.0);
+          const double jm = -__dmul_rn(G[a], uj[b]);
+          c += (__dadd_rn(__dadd_rn(jv, jr), jm) != 0.0);
+        }
+        c += (G[a] != 0.0);  // -(g G_a) block
+      }
+      for (int b = 0; b < 3; ++b) c += (__dmul_rn(D[b], Uj.w) != 0.0);
+      const double t = __dadd_rn(__dadd_rn(__dmul_rn(D[0], uj[0]), __dmul_rn(D[1], uj[1])),
+                                 __dmul_rn(D[2], uj[2]));
+      c += (__dadd_rn(__dadd_rn(0.0, df), -t) != 0.0);
+    }
+    if (per_row) per_row[i] = c;
+    r[0] += c;
+  }
+  grid_reduce<1>(grid, sm, r, part);
+  return r[0];
+}
+
+__device__ void set_status(int* st, int v) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *st = v;
+}
+
+template <class F>
+__device__ void pointwise(int64_t N, F f) {
+  int64_t lo, hi;
+  brange(N, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) f(i);
+}
+
+__device__ EngineTask base_task(const SweArgs& A) {
+  EngineTask T;
+  for (int l = 0; l < MAXV; ++l) T.v[l] = nullptr;
+  for (int l = 0; l < MAXNS; ++l) T.W[l] = nullptr;
+  T.tol = A.tol;
+  T.delta = 1.4;
+  T.tau_init = -1.0;
+  T.m_init = 1;
+  T.iom = 2;
+  T.m_max = 100;
+  T.max_attempts = 1000000;
+  T.zero_skip = 1;
+  return T;
+}
+
+// ---------------------------------------------------------------- step kernel
+// One whole integrator step (integrators.py:140-224) on the resident state.
+__global__ void __launch_bounds__(TPB) k_swe_step(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  SweOp S = A.S;
+  S.lin = A.u;
+  EngineWork Wk = A.Wk;
+  const double dt = A.dt;
+  int st = phase_rhs(grid, sm, S, A.u, A.fn, A.v1, dt, true, Wk.part);
+  if (st != EIK_OK) { set_status(A.status, st); return; }
+  Wk.nnz = (int64_t)phase_count_nnz(grid, sm, S, Wk.part);
+  SweOp SA = S;
+  SA.scale = dt;
+  const double4* u = A.u;
+  double4* Ub = A.Ub;
+  double4 *va = A.va, *vb = A.vb, *d2 = A.d2;
+  EngineTask T = base_task(A);
+  double4* fin = nullptr;      // W column added in the final combination
+  const double4* base = u;     // u_{n+1} = base + fin
+  switch (A.scheme) {
+    case EIK_RB_EULER: {
+      T.p = 1; T.v[1] = A.v1; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[0];
+      T.slot = EIK_SLOT_RBE; T.info_idx = 0;
+      st = engine_call(grid, sm, SA, T, Wk);
+      fin = A.W[0];
+      break;
+    }
+    case EIK_EPI3: {
+      const double c = (2.0 / 3.0) * dt;
+      st = phase_dev(grid, sm, S, A.uprev, A.fn,
+                     [&](int64_t i, double4 d) { va[i] = c * d; }, Wk.part);
+      if (st != EIK_OK) break;
+      T.p = 2; T.v[1] = A.v1; T.v[2] = va; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[0];
+      T.slot = EIK_SLOT_EPI3; T.info_idx = 0;
+      st = engine_call(grid, sm, SA, T, Wk);
+      fin = A.W[0];
+      break;
+    }
+    case EIK_EXPRB42: {
+      T.p = 1; T.v[1] = A.v1; T.ns = 1; T.rho[0] = 0.75; T.W[0] = A.W[0];
+      T.slot = EIK_SLOT_EXPRB42_1; T.info_idx = 0;
+      st = engine_call(grid, sm, SA, T, Wk);
+      if (st != EIK_OK) break;
+      double4* W0 = A.W[0];
+      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
+      grid.sync();
+      const double c = (32.0 / 9.0) * dt;
+      st = phase_dev(grid, sm, S, Ub, A.fn,
+                     [&](int64_t i, double4 d) { va[i] = c * d; }, Wk.part);
+      if (st != EIK_OK) break;
+      T = base_task(A);
+      T.p = 3; T.v[1] = A.v1; T.v[3] = va; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[1];
+      T.slot = EIK_SLOT_EXPRB42_2; T.info_idx = 1;
+      st = engine_call(grid, sm, SA, T, Wk);
+      fin = A.W[1];
+      break;
+    }
+    case EIK_PEXPRB43: {
+      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 1.0;
+      T.W[0] = A.W[0]; T.W[1] = A.W[1];
+      T.slot = EIK_SLOT_PEXPRB43_1; T.info_idx = 0;
+      st = engine_call(grid, sm, SA, T, Wk);
+      if (st != EIK_OK) break;
+      double4 *W0 = A.W[0], *W1 = A.W[1];
+      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
+      grid.sync();
+      st = phase_dev(grid, sm, S, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
+                     Wk.part);
+      if (st != EIK_OK) break;
+      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W1[i]; });  // U3
+      grid.sync();
+      st = phase_dev(grid, sm, S, Ub, A.fn,
+                     [&](int64_t i, double4 d3) {
+                       const double4 a = d2[i];
+                       va[i] = dt * ((16.0 * a) - (2.0 * d3));
+                       vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
+                     },
+                     Wk.part);
+      if (st != EIK_OK) break;
+      T = base_task(A);
+      T.p = 4; T.v[3] = va; T.v[4] = vb; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[2];
+      T.slot = EIK_SLOT_PEXPRB43_2; T.info_idx = 1;
+      st = engine_call(grid, sm, SA, T, Wk);
+      fin = A.W[2];
+      base = Ub;  // u_{n+1} = U3 + W2
+      break;
+    }
+    case EIK_EXPRB53: {
+      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+      T.W[0] = A.W[0]; T.W[1] = A.W[1];
+      T.slot = EIK_SLOT_EXPRB53_1; T.info_idx = 0;
+      st = engine_call(grid, sm, SA, T, Wk);
+      if (st != EIK_OK) break;
+      double4 *W0 = A.W[0], *W1 = A.W[1], *W2 = A.W[2], *W3 = A.W[3];
+      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
+      grid.sync();
+      st = phase_dev(grid, sm, S, Ub, A.fn,
+                     [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, Wk.part);
+      if (st != EIK_OK) break;
+      T = base_task(A);
+      T.p = 3; T.v[3] = va; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+      T.W[0] = W2; T.W[1] = W3;
+      T.slot = EIK_SLOT_EXPRB53_2; T.info_idx = 1;
+      st = engine_call(grid, sm, SA, T, Wk);
+      if (st != EIK_OK) break;
+      const double c1 = 27.0 / 25.0, c2 = 729.0 / 125.0, q3 = A.c09cube;
+      pointwise(S.N, [&](int64_t i) {
+        const double4 ph = make_double4(W2[i].x / 0.125, W2[i].y / 0.125,
+                                        W2[i].z / 0.125, W2[i].w / 0.125);
+        const double4 pn = make_double4(W3[i].x / q3, W3[i].y / q3, W3[i].z / q3,
+                                        W3[i].w / q3);
+        Ub[i] = ((u[i] + W1[i]) + c1 * ph) + c2 * pn;
+      });
+      grid.sync();
+      const double e1 = 250.0 / 81.0, e2 = 500.0 / 27.0;
+      st = phase_dev(grid, sm, S, Ub, A.fn,
+                     [&](int64_t i, double4 d3) {
+                       const double4 a = d2[i];
+                       va[i] = dt * ((18.0 * a) - (e1 * d3));
+                       vb[i] = dt * ((-60.0 * a) + (e2 * d3));
+                     },
+                     Wk.part);
+      if (st != EIK_OK) break;
+      T = base_task(A);
+      T.p = 4; T.v[1] = A.v1; T.v[3] = va; T.v[4] = vb; T.ns = 1; T.rho[0] = 1.0;
+      T.W[0] = A.W[4];
+      T.slot = EIK_SLOT_EXPRB53_3; T.info_idx = 2;
+      st = engine_call(grid, sm, SA, T, Wk);
+      fin = A.W[4];
+      break;
+    }
+    default:
+      st = EIK_EINVAL;
+  }
+  if (st == EIK_OK) {
+    double4* uu = A.u;
+    double4* up = A.uprev;
+    pointwise(S.N, [&](int64_t i) {
+      const double4 old = uu[i];
+      const double4 nb = base[i] + fin[i];
+      up[i] = old;
+      uu[i] = nb;
+    });
+  }
+  set_status(A.status, st);
+}
+
+// ------------------------------------------------------- API-level kernels
+__global__ void __launch_bounds__(TPB) k_swe_rhs(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  SweOp S = A.S;
+  S.lin = A.x;
+  int st = phase_rhs(grid, sm, S, A.x, A.out, nullptr, 0.0, false, A.Wk.part);
+  set_status(A.status, st);
+}
+
+__global__ void __launch_bounds__(TPB) k_swe_jv(SweArgs A) {
+  // A.x = linearisation state, A.va = direction, A.out = J v
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  SweOp S = A.S;
+  S.lin = A.x;
+  S.scale = 1.0;
+  int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  op_pre(S, A.va, 1.0, lo, hi);
+  grid.sync();
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) A.out[i] = op_main(S, A.va, i);
+  set_status(A.status, st);
+}
+
+__global__ void __launch_bounds__(TPB) k_swe_nnz(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  SweOp S = A.S;
+  S.lin = A.x;
+  int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  const double c = phase_count_nnz(grid, sm, S, A.Wk.part, A.dbg);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.nnz_out = c;
+  set_status(A.status, st);
+}
+
+__global__ void __launch_bounds__(TPB) k_swe_phipm(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  SweOp S = A.S;
+  S.lin = A.x;
+  int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  if (st != EIK_OK) { set_status(A.status, st); return; }
+  EngineWork Wk = A.Wk;
+  Wk.nnz = (int64_t)phase_count_nnz(grid, sm, S, Wk.part);
+  S.scale = A.dt;
+  st = engine_call(grid, sm, S, A.task, Wk);
+  set_status(A.status, st);
+}
+
+struct CsrArgs {
+  CsrOp C;
+  EngineWork Wk;
+  EngineTask task;
+  int* status;
+};
+
+__global__ void __launch_bounds__(TPB) k_csr_phipm(CsrArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const int st = engine_call(grid, sm, A.C, A.task, A.Wk);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = st;
+}
+
+// ====================================================================== host
+
+namespace {
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, count * sizeof(T) + 64);
+}
+
+struct Bufs {
+  std::vector<void*> ptrs;
+  template <class T>
+  cudaError_t get(T** p, size_t count) {
+    cudaError_t e = dalloc(p, count);
+    if (e == cudaSuccess) {
+      ptrs.push_back(*p);
+      e = cudaMemset(*p, 0, count * sizeof(T));
+    }
+    return e;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+int coop_grid(const void* const* kernels, int nk, int dev, int64_t NU) {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int best = 1 << 30;
+  for (int k = 0; k < nk; ++k) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernels[k], TPB, 0);
+    best = std::min(best, std::max(nb, 1) * nsm);
+  }
+  const int64_t need = (NU + TPB - 1) / TPB;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(best, need));
+}
+
+}  // namespace
+
+struct EngineHost {
+  Bufs mem;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int G = 1;
+  int64_t NU = 0, n = 0, m_alloc = 0;
+  EngineWork wk{};
+  double4* vin[MAXV] = {};
+  double4* wout[MAXNS] = {};
+  EikPhipmInfo* info_d = nullptr;
+  EikTraceRec* trace_d = nullptr;
+  int64_t trace_cap_d = 0;
+  int64_t* trace_len_d = nullptr;
+  int* status_d = nullptr;
+  double* nnz_d = nullptr;
+  unsigned long long* kiters_d = nullptr;
+  int64_t launches = 0;
+
+  eik_status init(int device, int64_t NU_, int64_t n_, int64_t m_alloc_,
+                  const void* const* kernels, int nk) {
+    dev = device;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    NU = NU_;
+    n = n_;
+    m_alloc = std::max<int64_t>(1, m_alloc_);
+    G = coop_grid(kernels, nk, dev, NU);
+    CK(mem.get(&wk.basis, (size_t)m_alloc * NU));
+    CK(mem.get(&wk.zbuf, NU));
+    for (int l = 1; l < MAXV; ++l) CK(mem.get(&wk.w[l], NU));
+    CK(mem.get(&wk.ybuf[0], NU));
+    CK(mem.get(&wk.ybuf[1], NU));
+    CK(mem.get(&wk.zero, NU));
+    CK(mem.get(&wk.part, (size_t)2 * G * NPART));
+    CK(mem.get(&wk.H, (size_t)m_alloc * m_alloc));
+    CK(mem.get(&wk.scr, (size_t)6 * MAXDIM * MAXDIM));
+    CK(mem.get(&wk.phi, MAXDIM + 4));
+    CK(mem.get(&wk.seeds, 2 * EIK_NUM_SLOTS));
+    CK(mem.get(&info_d, 4));
+    CK(mem.get(&trace_len_d, 1));
+    CK(mem.get(&status_d, 1));
+    CK(mem.get(&nnz_d, 1));
+    CK(mem.get(&kiters_d, 1));
+    wk.info = info_d;
+    wk.trace = nullptr;
+    wk.trace_cap = 0;
+    wk.trace_len = trace_len_d;
+    wk.kiters = kiters_d;
+    wk.NU = NU;
+    wk.n = n;
+    wk.m_alloc = m_alloc;
+    return reset_seeds();
+  }
+  eik_status reset_seeds() {
+    std::vector<double> s(2 * EIK_NUM_SLOTS);
+    for (int k = 0; k < EIK_NUM_SLOTS; ++k) {
+      s[2 * k] = -1.0;  // None
+      s[2 * k + 1] = 1.0;
+    }
+    CK(cudaMemcpy(wk.seeds, s.data(), s.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return EIK_OK;
+  }
+  eik_status ensure_io() {
+    if (vin[0]) return EIK_OK;
+    for (int l = 0; l < MAXV; ++l) CK(mem.get(&vin[l], NU));
+    for (int l = 0; l < MAXNS; ++l) CK(mem.get(&wout[l], NU));
+    return EIK_OK;
+  }
+  eik_status ensure_trace(int64_t cap) {
+    if (cap <= trace_cap_d) return EIK_OK;
+    if (trace_d) cudaFree(trace_d);
+    CK(dalloc(&trace_d, (size_t)cap));
+    trace_cap_d = cap;
+    return EIK_OK;
+  }
+  // validation mirroring PhiTask.__post_init__ (phipm.py:109-125)
+  eik_status check_task(const EikPhiTask* t) {
+    if (!t) return fail(EIK_EINVAL, "task is NULL");
+    if (t->p < 0 || t->p + 1 > MAXV)
+      return fail(EIK_EINVAL, "at least one input vector is required (p+1 <= 8)");
+    if (t->ns < 1 || t->ns > MAXNS || !t->rho)
+      return fail(EIK_EINVAL, "rho must lie in (0, 1]");
+    if (!(t->rho[0] > 0.0) || t->rho[t->ns - 1] > 1.0)
+      return fail(EIK_EINVAL, "rho must lie in (0, 1]");
+    for (int i = 1; i < t->ns; ++i)
+      if (!(t->rho[i] > t->rho[i - 1])) return fail(EIK_EINVAL, "rho must be strictly ascending");
+    if (!(t->tol > 0.0)) return fail(EIK_EINVAL, "tol must be positive");
+    if (t->iom < 1) return fail(EIK_EINVAL, "iom must be >= 1");
+    const int64_t mcap = std::min<int64_t>(std::max(t->m_max, 1), n);
+    if (mcap > m_alloc)
+      return fail(EIK_EINVAL, "m_max exceeds the context's basis allocation");
+    if (mcap + t->p + 1 > MAXDIM) return fail(EIK_EINVAL, "augmented dense size exceeds cap 256");
+    return EIK_OK;
+  }
+  EngineTask make_task(const EikPhiTask* t) {
+    EngineTask T;
+    memset(&T, 0, sizeof(T));
+    T.p = t->p;
+    T.ns = t->ns;
+    for (int i = 0; i < t->ns; ++i) T.rho[i] = t->rho[i];
+    for (int l = 0; l <= t->p; ++l) T.v[l] = (t->v && t->v[l]) ? vin[l] : nullptr;
+    for (int i = 0; i < t->ns; ++i) T.W[i] = wout[i];
+    T.tol = t->tol;
+    T.delta = t->delta;
+    T.tau_init = t->tau_init > 0.0 ? t->tau_init : -1.0;
+    T.m_init = t->m_init;
+    T.iom = t->iom;
+    T.m_max = t->m_max;
+    T.max_attempts = t->max_attempts > 0 ? t->max_attempts : 1000000;
+    T.zero_skip = t->zero_skip;
+    T.slot = -1;
+    T.info_idx = 0;
+    return T;
+  }
+  eik_status finish_phipm(EikPhipmInfo* info, EikTraceRec* trace, int64_t trace_cap,
+                          int64_t* trace_len) {
+    int sth = 0;
+    EikPhipmInfo inf;
+    CK(cudaMemcpyAsync(&sth, status_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&inf, info_d, sizeof(inf), cudaMemcpyDeviceToHost, st));
+    int64_t tl = 0;
+    CK(cudaMemcpyAsync(&tl, trace_len_d, sizeof(tl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (info) *info = inf;
+    if (trace && trace_cap > 0) {
+      const int64_t nrec = std::min(tl, trace_cap);
+      if (nrec > 0)
+        CK(cudaMemcpy(trace, trace_d, nrec * sizeof(EikTraceRec), cudaMemcpyDeviceToHost));
+      if (trace_len) *trace_len = tl;
+    } else if (trace_len) {
+      *trace_len = 0;
+    }
+    if (sth == EIK_EPHIPM) return fail(EIK_EPHIPM, "no convergence within the substep budget");
+    if (sth != EIK_OK) return fail((eik_status)sth, "engine failed");
+    return EIK_OK;
+  }
+  void release() {
+    if (trace_d) cudaFree(trace_d);
+    trace_d = nullptr;
+    mem.release();
+    if (st) cudaStreamDestroy(st);
+    st = nullptr;
+  }
+};
+
+struct EikSwe {
+  EngineHost eng;
+  int64_t N = 0;
+  int K = 0;
+  SweOp S{};
+  double4 *u = nullptr, *uprev = nullptr, *fn = nullptr, *v1 = nullptr, *va = nullptr,
+          *vb = nullptr, *d2 = nullptr, *Ub = nullptr, *W[5] = {}, *x = nullptr,
+          *out = nullptr;
+  double* soa = nullptr;
+  bool have_prev = false;
+  double c09cube = 0.0;
+  // graph cache for eik_swe_step
+  cudaGraphExec_t gexec = nullptr;
+  int g_scheme = -1;
+  double g_dt = 0.0, g_tol = 0.0;
+  bool graphs_ok = true;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.0f;
+  double* pinned = nullptr;  // pinned staging for host copies (4N doubles)
+
+  SweArgs args() {
+    SweArgs A;
+    memset(&A, 0, sizeof(A));
+    A.S = S;
+    A.Wk = eng.wk;
+    A.u = u;
+    A.uprev = uprev;
+    A.fn = fn;
+    A.v1 = v1;
+    A.va = va;
+    A.vb = vb;
+    A.d2 = d2;
+    A.Ub = Ub;
+    for (int k = 0; k < 5; ++k) A.W[k] = W[k];
+    A.x = x;
+    A.out = out;
+    A.c09cube = c09cube;
+    A.status = eng.status_d;
+    A.nnz_out = eng.nnz_d;
+    return A;
+  }
+  eik_status launch(const void* fn_, SweArgs& A) {
+    void* kargs[] = {&A};
+    CK(cudaLaunchCooperativeKernel(fn_, eng.G, TPB, kargs, 0, eng.st));
+    ++eng.launches;
+    return EIK_OK;
+  }
+  eik_status h2d_cells(const double* h, double4* d) {
+    CK(cudaMemcpyAsync(soa, h, 4 * N * sizeof(double), cudaMemcpyHostToDevice, eng.st));
+    k_soa_to_cell<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(soa, d, N);
+    ++eng.launches;
+    CK(cudaGetLastError());
+    return EIK_OK;
+  }
+  eik_status d2h_cells(const double4* d, double* h) {
+    k_cell_to_soa<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(d, soa, N);
+    ++eng.launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, soa, 4 * N * sizeof(double), cudaMemcpyDeviceToHost, eng.st));
+    CK(cudaStreamSynchronize(eng.st));
+    return EIK_OK;
+  }
+  eik_status status() {
+    int sth = 0;
+    CK(cudaMemcpyAsync(&sth, eng.status_d, sizeof(int), cudaMemcpyDeviceToHost, eng.st));
+    CK(cudaStreamSynchronize(eng.st));
+    if (sth == EIK_ENONFINITE) return fail(EIK_ENONFINITE, "non-finite right-hand side");
+    if (sth == EIK_EPHIPM) return fail(EIK_EPHIPM, "no convergence within the substep budget");
+    if (sth != EIK_OK) return fail((eik_status)sth, "device step failed");
+    return EIK_OK;
+  }
+};
+
+struct EikCsr {
+  EngineHost eng;
+  CsrOp C{};
+  int64_t nnz = 0;
+};
+
+static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_rhs,
+                                    (const void*)k_swe_jv, (const void*)k_swe_nnz,
+                                    (const void*)k_swe_phipm};
+static const void* kCsrKernels[] = {(const void*)k_csr_phipm};
+
+extern "C" {
+
+const char* eik_last_error(void) { return g_err.c_str(); }
+int eik_version(void) { return 1; }
+
+eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
+                          const double* n_y, const double* n_z, const double* f,
+                          const double* h_s, double g, double nu, int32_t device,
+                          int32_t m_max, EikSwe** out) {
+  if (!out || !ops || n_g < 1 || !n_x || !n_y || !n_z || !f || !h_s)
+    return fail(EIK_EINVAL, "invalid arguments to eik_swe_create");
+  const int64_t N = n_g;
+  // ---- union stencil per row, ELL coefficients.  Slots follow the sorted
+  // column order of the CSR rows (self included at its sorted position) so
+  // that sequential slot sums reproduce scipy's csr_matvec order exactly.
+  std::vector<std::vector<int32_t>> cols(N);
+  for (int64_t i = 0; i < N; ++i) cols[i].push_back((int32_t)i);
+  for (int o = 0; o < NOPS; ++o) {
+    const EikCsrView& M = ops[o];
+    if (!M.indptr || (M.nnz > 0 && (!M.indices || !M.data)))
+      return fail(EIK_EINVAL, "operator CSR arrays missing");
+    if (M.indptr[N] != M.nnz) return fail(EIK_EINVAL, "operator indptr/nnz mismatch");
+    for (int64_t i = 0; i < N; ++i)
+      for (int32_t k = M.indptr[i]; k < M.indptr[i + 1]; ++k) {
+        const int32_t j = M.indices[k];
+        if (j < 0 || j >= N) return fail(EIK_EINVAL, "column index out of range");
+        if (!std::isfinite(M.data[k])) return fail(EIK_EINVAL, "SparseMatrix entries must be finite");
+        auto& c = cols[i];
+        if (std::find(c.begin(), c.end(), j) == c.end()) c.push_back(j);
+      }
+  }
+  int K = 1;
+  for (int64_t i = 0; i < N; ++i) {
+    std::sort(cols[i].begin(), cols[i].end());
+    K = std::max<int>(K, (int)cols[i].size());
+  }
+  if (K > KMAX) return fail(EIK_EINVAL, "stencil wider than 8 points per row");
+  std::vector<int32_t> nbr((size_t)K * N), cnt(N), dfx(N, 0);
+  std::vector<double> coef((size_t)K * NOPS * N, 0.0), df1((size_t)K * N, 0.0);
+  for (int64_t i = 0; i < N; ++i) {
+    cnt[i] = (int32_t)cols[i].size();
+    for (int s = 0; s < K; ++s)
+      nbr[(size_t)s * N + i] = s < cnt[i] ? cols[i][s] : (int32_t)i;
+  }
+  auto slot_of = [&](int64_t i, int32_t j) -> int {
+    const auto& c = cols[i];
+    auto it = std::lower_bound(c.begin(), c.end(), j);
+    if (it != c.end() && *it == j) return (int)(it - c.begin());
+    return -1;
+  };
+  for (int o = 0; o < NOPS; ++o) {
+    const EikCsrView& M = ops[o];
+    for (int64_t i = 0; i < N; ++i)
+      for (int32_t k = M.indptr[i]; k < M.indptr[i + 1]; ++k) {
+        const int s = slot_of(i, M.indices[k]);
+        coef[((size_t)s * NOPS + o) * N + i] += M.data[k];
+      }
+  }
+  {
+    const EikCsrView& Df = ops[10];
+    if (!Df.indptr || Df.indptr[N] != Df.nnz)
+      return fail(EIK_EINVAL, "Df CSR arrays missing or inconsistent");
+    for (int64_t i = 0; i < N; ++i)
+      for (int32_t k = Df.indptr[i]; k < Df.indptr[i + 1]; ++k) {
+        const int s = slot_of(i, Df.indices[k]);
+        if (s >= 0) df1[(size_t)s * N + i] += Df.data[k];
+        else if (Df.data[k] != 0.0) dfx[i] += 1;
+      }
+  }
+  EikSwe* c = new EikSwe();
+  c->N = N;
+  c->K = K;
+  c->c09cube = std::pow(0.9, 3.0);
+  eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
+                             kSweKernels, 5);
+  if (s != EIK_OK) { c->eng.release(); delete c; return s; }
+  Bufs& B = c->eng.mem;
+  int *d_nbr, *d_dfx, *d_cnt;
+  double *d_coef, *d_df1, *d_hs;
+  double4* d_nf;
+#define CKC(call)                                                              \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      c->eng.release();                                                        \
+      delete c;                                                                \
+      return fail(EIK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                          \
+  } while (0)
+  CKC(B.get(&d_nbr, (size_t)K * N));
+  CKC(B.get(&d_coef, (size_t)K * NOPS * N));
+  CKC(B.get(&d_df1, (size_t)K * N));
+  CKC(B.get(&d_dfx, N));
+  CKC(B.get(&d_cnt, N));
+  CKC(B.get(&d_hs, N));
+  CKC(B.get(&d_nf, N));
+  CKC(cudaMemcpy(d_nbr, nbr.data(), nbr.size() * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_coef, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_df1, df1.data(), df1.size() * 8, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_dfx, dfx.data(), dfx.size() * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_cnt, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_hs, h_s, N * 8, cudaMemcpyHostToDevice));
+  {
+    std::vector<double4> nf(N);
+    for (int64_t i = 0; i < N; ++i) nf[i] = make_double4(n_x[i], n_y[i], n_z[i], f[i]);
+    CKC(cudaMemcpy(d_nf, nf.data(), N * sizeof(double4), cudaMemcpyHostToDevice));
+  }
+  CKC(B.get(&c->u, N));
+  CKC(B.get(&c->uprev, N));
+  CKC(B.get(&c->fn, N));
+  CKC(B.get(&c->v1, N));
+  CKC(B.get(&c->va, N));
+  CKC(B.get(&c->vb, N));
+  CKC(B.get(&c->d2, N));
+  CKC(B.get(&c->Ub, N));
+  for (int k = 0; k < 5; ++k) CKC(B.get(&c->W[k], N));
+  CKC(B.get(&c->x, N));
+  CKC(B.get(&c->out, N));
+  CKC(B.get(&c->soa, 4 * N));
+  double4 *ne, *lapA, *lapB;
+  CKC(B.get(&ne, N));
+  CKC(B.get(&lapA, N));
+  CKC(B.get(&lapB, N));
+  CKC(cudaEventCreate(&c->ev0));
+  CKC(cudaEventCreate(&c->ev1));
+#undef CKC
+  SweOp& S = c->S;
+  S.N = N;
+  S.K = K;
+  S.nbr = d_nbr;
+  S.coef = d_coef;
+  S.nf = d_nf;
+  S.hs = d_hs;
+  S.g = g;
+  S.nu = nu;
+  S.lin = c->u;
+  S.ne = ne;
+  S.lapA = lapA;
+  S.lapB = lapB;
+  S.scale = 1.0;
+  S.df1 = d_df1;
+  S.dfx = d_dfx;
+  S.cnt = d_cnt;
+  *out = c;
+  return EIK_OK;
+}
+
+eik_status eik_swe_destroy(EikSwe* c) {
+  if (!c) return EIK_OK;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  c->eng.release();
+  delete c;
+  return EIK_OK;
+}
+
+eik_status eik_swe_set_state(EikSwe* c, const double* u) {
+  if (!c || !u) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->u);
+  if (s != EIK_OK) return s;
+  CK(cudaStreamSynchronize(c->eng.st));
+  return EIK_OK;
+}
+
+eik_status eik_swe_get_state(EikSwe* c, double* u) {
+  if (!c || !u) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  return c->d2h_cells(c->u, u);
+}
+
+eik_status eik_swe_set_prev(EikSwe* c, const double* u_prev) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  if (!u_prev) {
+    c->have_prev = false;
+    return EIK_OK;
+  }
+  eik_status s = c->h2d_cells(u_prev, c->uprev);
+  if (s != EIK_OK) return s;
+  CK(cudaStreamSynchronize(c->eng.st));
+  c->have_prev = true;
+  return EIK_OK;
+}
+
+eik_status eik_swe_rhs(EikSwe* c, const double* u, double* out) {
+  if (!c || !u || !out) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->x);
+  if (s != EIK_OK) return s;
+  SweArgs A = c->args();
+  if ((s = c->launch((const void*)k_swe_rhs, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  return c->d2h_cells(c->out, out);
+}
+
+eik_status eik_swe_jv(EikSwe* c, const double* u, const double* v, double* out) {
+  if (!c || !u || !v || !out) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->x);
+  if (s == EIK_OK) s = c->h2d_cells(v, c->va);
+  if (s != EIK_OK) return s;
+  SweArgs A = c->args();
+  if ((s = c->launch((const void*)k_swe_jv, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  return c->d2h_cells(c->out, out);
+}
+
+eik_status eik_swe_jac_nnz_rows(EikSwe* c, const double* u, int64_t* nnz,
+                                double* per_cell) {
+  if (!c || !u || !nnz) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->x);
+  if (s != EIK_OK) return s;
+  SweArgs A = c->args();
+  A.dbg = per_cell ? c->soa : nullptr;
+  if ((s = c->launch((const void*)k_swe_nnz, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  double v = 0.0;
+  CK(cudaMemcpy(&v, c->eng.nnz_d, sizeof(double), cudaMemcpyDeviceToHost));
+  *nnz = (int64_t)v;
+  if (per_cell) CK(cudaMemcpy(per_cell, c->soa, c->N * sizeof(double), cudaMemcpyDeviceToHost));
+  return EIK_OK;
+}
+
+eik_status eik_swe_jac_nnz(EikSwe* c, const double* u, int64_t* nnz) {
+  if (!c || !u || !nnz) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->x);
+  if (s != EIK_OK) return s;
+  SweArgs A = c->args();
+  if ((s = c->launch((const void*)k_swe_nnz, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  double v = 0.0;
+  CK(cudaMemcpy(&v, c->eng.nnz_d, sizeof(double), cudaMemcpyDeviceToHost));
+  *nnz = (int64_t)v;
+  return EIK_OK;
+}
+
+eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
+                         const EikPhiTask* task, double* W, EikPhipmInfo* info,
+                         EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (!c || !u_lin || !W) return fail(EIK_EINVAL, "invalid arguments");
+  EngineHost& E = c->eng;
+  eik_status s = E.check_task(task);
+  if (s != EIK_OK) return s;
+  CK(cudaSetDevice(E.dev));
+  if ((s = E.ensure_io()) != EIK_OK) return s;
+  if ((s = c->h2d_cells(u_lin, c->x)) != EIK_OK) return s;
+  for (int l = 0; l <= task->p; ++l)
+    if (task->v && task->v[l] && (s = c->h2d_cells(task->v[l], E.vin[l])) != EIK_OK) return s;
+  if (trace && trace_cap > 0 && (s = E.ensure_trace(trace_cap)) != EIK_OK) return s;
+  SweArgs A = c->args();
+  A.dt = dt;
+  A.task = E.make_task(task);
+  A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
+  A.Wk.trace_cap = (trace && trace_cap > 0) ? trace_cap : 0;
+  CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
+  if ((s = c->launch((const void*)k_swe_phipm, A)) != EIK_OK) return s;
+  s = E.finish_phipm(info, trace, trace_cap, trace_len);
+  if (s != EIK_OK) return s;
+  for (int i = 0; i < task->ns; ++i)
+    if ((s = c->d2h_cells(E.wout[i], W + (size_t)i * 4 * c->N)) != EIK_OK) return s;
+  return EIK_OK;
+}
+
+static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol) {
+  SweArgs A = c->args();
+  A.dt = dt;
+  A.tol = tol;
+  A.scheme = scheme;
+  if (c->graphs_ok) {
+    if (!c->gexec || c->g_scheme != scheme || c->g_dt != dt || c->g_tol != tol) {
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(c->eng.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        void* kargs[] = {&A};
+        ok = cudaLaunchCooperativeKernel((const void*)k_swe_step, c->eng.G, TPB, kargs, 0,
+                                         c->eng.st) == cudaSuccess;
+        ok = (cudaStreamEndCapture(c->eng.st, &graph) == cudaSuccess) && ok;
+      }
+      if (ok) ok = cudaGraphInstantiate(&c->gexec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {
+        cudaGetLastError();
+        c->graphs_ok = false;
+        c->gexec = nullptr;
+      } else {
+        c->g_scheme = scheme;
+        c->g_dt = dt;
+        c->g_tol = tol;
+      }
+    }
+    if (c->graphs_ok) {
+      CK(cudaGraphLaunch(c->gexec, c->eng.st));
+      ++c->eng.launches;
+      return EIK_OK;
+    }
+  }
+  return c->launch((const void*)k_swe_step, A);
+}
+
+eik_status eik_swe_step(EikSwe* c, int32_t scheme, double dt, double tol,
+                        EikPhipmInfo* calls, int32_t* ncalls) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  if (!(dt > 0.0)) return fail(EIK_EINVAL, "dt must be positive");
+  if (scheme < 0 || scheme > EIK_EXPRB53) return fail(EIK_EINVAL, "unknown scheme");
+  if (scheme == EIK_EPI3 && !c->have_prev)
+    return fail(EIK_EINVAL, "epi3 requires the previous state");
+  CK(cudaSetDevice(c->eng.dev));
+  CK(cudaEventRecord(c->ev0, c->eng.st));
+  eik_status s = step_enqueue(c, scheme, dt, tol);
+  if (s != EIK_OK) return s;
+  CK(cudaEventRecord(c->ev1, c->eng.st));
+  EikPhipmInfo inf[4];
+  CK(cudaMemcpyAsync(inf, c->eng.info_d, sizeof(inf), cudaMemcpyDeviceToHost, c->eng.st));
+  s = c->status();
+  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  const int nc = scheme == EIK_EXPRB53 ? 3 : (scheme >= EIK_EXPRB42 ? 2 : 1);
+  if (calls)
+    for (int k = 0; k < nc; ++k) calls[k] = inf[k];
+  if (ncalls) *ncalls = nc;
+  if (s == EIK_OK) c->have_prev = true;
+  return s;
+}
+
+eik_status eik_swe_advance(EikSwe* c, int32_t scheme, double dt, double tol,
+                           int32_t nsteps, int64_t* matvecs, int64_t* substeps) {
+  if (!c || nsteps < 0) return fail(EIK_EINVAL, "invalid arguments");
+  if (scheme == EIK_EPI3 && !c->have_prev)
+    return fail(EIK_EINVAL, "epi3 requires the previous state");
+  int64_t mv = 0, ss = 0;
+  for (int k = 0; k < nsteps; ++k) {
+    EikPhipmInfo calls[3];
+    int32_t nc = 0;
+    eik_status s = eik_swe_step(c, scheme, dt, tol, calls, &nc);
+    if (s != EIK_OK) return s;
+    for (int q = 0; q < nc; ++q) {
+      mv += calls[q].matvecs;
+      ss += calls[q].substeps;
+    }
+  }
+  if (matvecs) *matvecs = mv;
+  if (substeps) *substeps = ss;
+  return EIK_OK;
+}
+
+eik_status eik_swe_seeds(EikSwe* c, int32_t slot, double* tau, int64_t* m, int32_t set) {
+  if (!c || slot < 0 || slot >= EIK_NUM_SLOTS || !tau || !m)
+    return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  double v[2];
+  if (set) {
+    v[0] = *tau > 0.0 ? *tau : -1.0;
+    v[1] = (double)*m;
+    CK(cudaMemcpy(c->eng.wk.seeds + 2 * slot, v, sizeof(v), cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(v, c->eng.wk.seeds + 2 * slot, sizeof(v), cudaMemcpyDeviceToHost));
+    *tau = v[0];
+    *m = (int64_t)v[1];
+  }
+  return EIK_OK;
+}
+
+eik_status eik_swe_reset_seeds(EikSwe* c) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  return c->eng.reset_seeds();
+}
+
+int64_t eik_swe_launches(const EikSwe* c) { return c ? c->eng.launches : 0; }
+double eik_swe_last_kernel_ms(const EikSwe* c) { return c ? (double)c->last_ms : 0.0; }
+int64_t eik_swe_krylov_iters(const EikSwe* c) {
+  if (!c) return 0;
+  unsigned long long v = 0;
+  cudaMemcpy(&v, c->eng.kiters_d, sizeof(v), cudaMemcpyDeviceToHost);
+  return (int64_t)v;
+}
+
+// ------------------------------------------------------------------ CSR
+eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max,
+                          EikCsr** out) {
+  if (!out || n < 1 || !A.indptr || A.indptr[n] != A.nnz)
+    return fail(EIK_EINVAL, "invalid CSR operator");
+  for (int64_t k = 0; k < A.nnz; ++k) {
+    if (A.indices[k] < 0 || A.indices[k] >= n) return fail(EIK_EINVAL, "column index out of range");
+    if (!std::isfinite(A.data[k])) return fail(EIK_EINVAL, "SparseMatrix entries must be finite");
+  }
+  EikCsr* c = new EikCsr();
+  const int64_t NU = (n + 3) / 4;
+  eik_status s = c->eng.init(device, NU, n, std::min<int64_t>(std::max(m_max, 1), n),
+                             kCsrKernels, 1);
+  if (s != EIK_OK) { c->eng.release(); delete c; return s; }
+  int *rp, *ci;
+  double* val;
+  Bufs& B = c->eng.mem;
+  if (B.get(&rp, n + 1) != cudaSuccess || B.get(&ci, std::max<int64_t>(A.nnz, 1)) != cudaSuccess ||
+      B.get(&val, std::max<int64_t>(A.nnz, 1)) != cudaSuccess) {
+    c->eng.release();
+    delete c;
+    return fail(EIK_ENOMEM, "device allocation failed");
+  }
+  cudaMemcpy(rp, A.indptr, (n + 1) * 4, cudaMemcpyHostToDevice);
+  if (A.nnz) {
+    cudaMemcpy(ci, A.indices, A.nnz * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(val, A.data, A.nnz * 8, cudaMemcpyHostToDevice);
+  }
+  c->C.n = n;
+  c->C.NUu = NU;
+  c->C.rp = rp;
+  c->C.ci = ci;
+  c->C.val = val;
+  c->C.scale = 1.0;
+  c->nnz = A.nnz;
+  *out = c;
+  return EIK_OK;
+}
+
+eik_status eik_csr_destroy(EikCsr* c) {
+  if (!c) return EIK_OK;
+  c->eng.release();
+  delete c;
+  return EIK_OK;
+}
+
+eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
+                         const EikPhiTask* task, double* W, EikPhipmInfo* info,
+                         EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (!c || !W) return fail(EIK_EINVAL, "invalid arguments");
+  EngineHost& E = c->eng;
+  eik_status s = E.check_task(task);
+  if (s != EIK_OK) return s;
+  CK(cudaSetDevice(E.dev));
+  if ((s = E.ensure_io()) != EIK_OK) return s;
+  const int64_t n = E.n;
+  for (int l = 0; l <= task->p; ++l) {
+    CK(cudaMemsetAsync(E.vin[l], 0, E.NU * sizeof(double4), E.st));
+    if (task->v && task->v[l])
+      CK(cudaMemcpyAsync(E.vin[l], task->v[l], n * sizeof(double), cudaMemcpyHostToDevice, E.st));
+  }
+  if (trace && trace_cap > 0 && (s = E.ensure_trace(trace_cap)) != EIK_OK) return s;
+  CsrArgs A;
+  memset(&A, 0, sizeof(A));
+  A.C = c->C;
+  A.C.scale = scale;
+  A.Wk = E.wk;
+  A.Wk.nnz = nnz_override >= 0 ? nnz_override : c->nnz;
+  A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
+  A.Wk.trace_cap = (trace && trace_cap > 0) ? trace_cap : 0;
+  A.task = E.make_task(task);
+  A.status = E.status_d;
+  CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
+  void* kargs[] = {&A};
+  CK(cudaLaunchCooperativeKernel((const void*)k_csr_phipm, E.G, TPB, kargs, 0, E.st));
+  ++E.launches;
+  s = E.finish_phipm(info, trace, trace_cap, trace_len);
+  if (s != EIK_OK) return s;
+  for (int i = 0; i < task->ns; ++i)
+    CK(cudaMemcpyAsync(W + (size_t)i * n, E.wout[i], n * sizeof(double), cudaMemcpyDeviceToHost, E.st));
+  CK(cudaStreamSynchronize(E.st));
+  return EIK_OK;
+}
+
+}  // extern "C"

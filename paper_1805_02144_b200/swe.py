@@ -1,0 +1,220 @@
+"""Shallow-water F(u), J(u) v and nnz(J) on the GPU, reference API.
+
+Mirrors /root/reference/pkg/src/expintkit/swe.py: ``DiscreteOperators``
+(23-46), ``split_state``/``stack_state`` (124-133), ``rhs`` (149-168),
+``assemble_jacobian`` (220-223; here a device operator: matrix-free J v plus
+the exact scipy nnz), ``dissipation_coefficient`` (65-67).  One ``SweContext``
+(C-ABI ``EikSwe``) is created per operator set and cached; it owns the
+device copy of the grid (ELL stencil built from the CSR operators), the
+resident trajectory state and the engine's warm-start seeds.
+"""
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from . import _native as nat
+from .grid import DiscreteOperators, dissipation_coefficient  # noqa: F401
+from .phipm import DeviceOperator, MatvecOperator
+
+_OP_ORDER = ("Gx", "Gy", "Gz", "Dx", "Dy", "Dz", "Vx", "Vy", "Vz", "L", "Df")
+
+
+def split_state(ops, state):
+    n = ops.n_g
+    state = np.asarray(state, dtype=float)
+    if state.shape != (4 * n,):
+        raise ValueError(f"state must have length {4 * n}")
+    return state[:n], state[n:2 * n], state[2 * n:3 * n], state[3 * n:]
+
+
+def stack_state(ux, uy, uz, h):
+    return np.concatenate([ux, uy, uz, h])
+
+
+class SweContext:
+    """Device context for one operator set (owns an ``EikSwe``)."""
+
+    def __init__(self, ops, device=0, m_max=100):
+        lib = nat.load()
+        self.ops = ops
+        self.n_g = int(ops.n_g)
+        self.n = 4 * self.n_g
+        views = (nat.EikCsrView * 11)()
+        keep = []
+        for k, name in enumerate(_OP_ORDER):
+            v, kp = nat.csr_view(getattr(ops, name))
+            views[k] = v
+            keep.append(kp)
+        fields = [np.ascontiguousarray(getattr(ops, f), dtype=float)
+                  for f in ("n_x", "n_y", "n_z", "f", "h_s")]
+        h = C.c_void_p()
+        st = lib.eik_swe_create(self.n_g, views, *(nat.dptr(a) for a in fields),
+                                float(ops.g), float(ops.nu), int(device),
+                                int(m_max), C.byref(h))
+        nat.check(st, "eik_swe_create")
+        self.h = h
+        self._fin = weakref.finalize(self, lib.eik_swe_destroy, h)
+
+    # --------------------------------------------------------------- basics
+    def _vec(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError(f"state must have length {self.n}")
+        return x
+
+    def rhs(self, u):
+        u = self._vec(u)
+        out = np.empty(self.n)
+        nat.check(nat.load().eik_swe_rhs(self.h, nat.dptr(u), nat.dptr(out)),
+                  "rhs")
+        return out
+
+    def jv(self, u, v):
+        u, v = self._vec(u), self._vec(v)
+        out = np.empty(self.n)
+        nat.check(nat.load().eik_swe_jv(self.h, nat.dptr(u), nat.dptr(v),
+                                        nat.dptr(out)), "J v")
+        return out
+
+    def jac_nnz(self, u):
+        u = self._vec(u)
+        r = C.c_int64(0)
+        nat.check(nat.load().eik_swe_jac_nnz(self.h, nat.dptr(u), C.byref(r)),
+                  "nnz(J)")
+        return int(r.value)
+
+    def set_state(self, u):
+        u = self._vec(u)
+        nat.check(nat.load().eik_swe_set_state(self.h, nat.dptr(u)), "set_state")
+
+    def get_state(self):
+        out = np.empty(self.n)
+        nat.check(nat.load().eik_swe_get_state(self.h, nat.dptr(out)),
+                  "get_state")
+        return out
+
+    def set_prev(self, u_prev):
+        if u_prev is None:
+            nat.check(nat.load().eik_swe_set_prev(self.h, None), "set_prev")
+            return
+        u = self._vec(u_prev)
+        nat.check(nat.load().eik_swe_set_prev(self.h, nat.dptr(u)), "set_prev")
+
+    def step(self, scheme, dt, tol):
+        """One resident-state step; returns the per-engine-call infos."""
+        calls = (nat.EikPhipmInfo * 3)()
+        nc = C.c_int32(0)
+        st = nat.load().eik_swe_step(self.h, nat.SCHEME_IDS[scheme], float(dt),
+                                     float(tol), calls, C.byref(nc))
+        if st == nat.EIK_EPHIPM:
+            from .phipm import PhipmFailure
+            bad = [c for c in calls[:nc.value] if c.status == nat.EIK_EPHIPM]
+            c = bad[0] if bad else calls[0]
+            raise PhipmFailure("no convergence within the substep budget",
+                               t_reached=c.t_reached, substeps=c.substeps,
+                               rejections=c.rejections, matvecs=c.matvecs)
+        nat.check(st, f"step {scheme}")
+        return [calls[k] for k in range(nc.value)]
+
+    def seeds(self, slot):
+        tau = C.c_double(0.0)
+        m = C.c_int64(0)
+        nat.check(nat.load().eik_swe_seeds(self.h, nat.SLOT_IDS[slot],
+                                           C.byref(tau), C.byref(m), 0), "seeds")
+        return (tau.value if tau.value > 0 else None), int(m.value)
+
+    def set_seeds(self, slot, tau, m):
+        t = C.c_double(tau if tau else -1.0)
+        mm = C.c_int64(int(m))
+        nat.check(nat.load().eik_swe_seeds(self.h, nat.SLOT_IDS[slot],
+                                           C.byref(t), C.byref(mm), 1), "seeds")
+
+    def reset_seeds(self):
+        nat.check(nat.load().eik_swe_reset_seeds(self.h), "reset_seeds")
+
+    def launches(self):
+        return int(nat.load().eik_swe_launches(self.h))
+
+    def krylov_iters(self):
+        return int(nat.load().eik_swe_krylov_iters(self.h))
+
+    def last_kernel_ms(self):
+        return float(nat.load().eik_swe_last_kernel_ms(self.h))
+
+
+_CTX = {}
+
+
+def context(ops):
+    """The cached SweContext of an operator set."""
+    key = id(ops)
+    ent = _CTX.get(key)
+    if ent is not None and ent[0]() is ops:
+        return ent[1]
+    ctx = SweContext(ops)
+    try:
+        ref = weakref.ref(ops, lambda _r, k=key: _CTX.pop(k, None))
+    except TypeError:
+        ref = (lambda o: (lambda: o))(ops)
+    _CTX[key] = (ref, ctx)
+    return ctx
+
+
+def rhs(ops, state):
+    """Tendency of [u_x; u_y; u_z; h] (swe.py:149-168), computed on the GPU.
+    Raises ValueError on a non-finite state or tendency."""
+    return context(ops).rhs(state)
+
+
+class SweJacobian(DeviceOperator):
+    """J(u) (swe.py:175-223) as a device operator: ``matvec`` runs the
+    matrix-free stencil J v on the GPU and ``nnz`` is the exact nnz the
+    reference's assembled scipy CSR would have (the engine's n_A)."""
+
+    kind = "swe"
+
+    def __init__(self, ops, state, scale=1.0, _nnz=None):
+        self.ctx = context(ops)
+        self.state = np.ascontiguousarray(state, dtype=float).copy()
+        if not np.all(np.isfinite(self.state)):
+            raise ValueError("state must be finite")
+        self.n = self.ctx.n
+        self.n_rows = self.n
+        self.scale = float(scale)
+        self._nnz = _nnz
+
+    @property
+    def nnz(self):
+        if self._nnz is None:
+            self._nnz = self.ctx.jac_nnz(self.state)
+        return self._nnz
+
+    def matvec(self, x):
+        out = self.ctx.jv(self.state, x)
+        return out if self.scale == 1.0 else self.scale * out
+
+    def scaled(self, alpha):
+        return SweJacobian(self.ctx.ops, self.state, self.scale * float(alpha),
+                           self._nnz)
+
+    def as_matvec_operator(self):
+        op = MatvecOperator(self.matvec, self.n, self.nnz)
+        op.device = self
+        return op
+
+    def run_phipm(self, task, W, info, trace, cap, tlen):
+        u = self.state
+        return nat.load().eik_swe_phipm(
+            self.ctx.h, nat.dptr(u), self.scale, C.byref(task), nat.dptr(W),
+            C.byref(info), trace, cap, C.byref(tlen))
+
+
+def assemble_jacobian(ops, state):
+    """Full 4N x 4N tendency Jacobian as a device operator."""
+    return SweJacobian(ops, state)
+
+
+def jacobian_nnz(ops, state):
+    return context(ops).jac_nnz(state)
