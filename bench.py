@@ -1,0 +1,306 @@
+"""Benchmark: EXPRB4 steps/s at 655k cells (fp64) on B200, plus the
+J*v+IOM2 roofline -- BASELINE.json's metric on config C3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config C3] [--scheme exprb42] [--no-cpu-baseline]
+
+One process per GPU (torchrun for N > 1).  The path does not shard (SURVEY.md
+§8e: replicas only): every rank integrates its own trajectory of the same
+workload on its own GPU, with no data-path collective; ``value`` is the sum of
+steps over ranks divided by the max-over-ranks device time ("weak" scaling).
+
+A step is one EXPRB4 step of the resident state: F(u_n), eta, n_A, two
+phipm/IOM2 engine calls, the stage perturbation -- one cooperative kernel per
+step (libeik ``k_swe_step``), CUDA-graph replayed.  Timing: CUDA events
+recorded by libeik around every step kernel on its stream, barrier +
+device synchronise before and after the timed loop.  Each Krylov iteration
+streams ~0.5 GB, far more than the 126 MB L2, so no explicit flush is done.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy/scipy oracle port in oracle/, the reference itself being Python that
+cannot travel to the GPU box) on the host cores, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EXPRB4 steps/s at 655k cells fp64; J*v+IOM2 achieved HBM GB/s vs peak"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--scheme", default="exprb42")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+def b_alg_per_iter(ops):
+    """N*(96+64+24) + 8*W_coef, W_coef = nnz of the distinct
+    CSR arrays among Gx..Vz, L."""
+    seen, wc = [], 0
+    for name in ("Gx", "Gy", "Gz", "Dx", "Dy", "Dz", "Vx", "Vy", "Vz", "L"):
+        c = getattr(ops, name).csr
+        key = (c.nnz, c.data[:8].tobytes(), c.data[-8:].tobytes() if c.nnz else b"")
+        if key in seen:
+            continue
+        seen.append(key)
+        wc += c.nnz
+    return ops.n_g * (96 + 64 + 24) + 8 * wc
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.tmp = None
+
+    def start(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.tmp.flush()
+        with open(self.tmp.name) as fh:
+            lines = [l.strip() for l in fh if l.strip()]
+        os.unlink(self.tmp.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline_oracle(ops, u0, spec, nsteps):
+    """The oracle port (numpy/scipy restatement of the reference) on the host
+    cores: ``nsteps`` steps from the config's initial state."""
+    from oracle import integrate_oracle, swe_problem
+    t = time.perf_counter()
+    integrate_oracle(swe_problem(ops), spec.scheme if spec.scheme else "exprb42", u0,
+                     spec.dt, nsteps * spec.dt, tol=spec.tol)
+    return time.perf_counter() - t
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = str(threads)
+    from paper_1805_02144_b200.states import make_config
+    ops, u0, spec = make_config(args.config)
+    spec.scheme = args.scheme
+    nsteps = max(1, min(args.steps, 2))
+    secs = cpu_baseline_oracle(ops, u0, spec, nsteps)
+    value = nsteps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+        "n_gpus": ws, "steps": nsteps, "warmup": 0, "ms_per_step": 1e3 * secs / nsteps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: L{ops.level} ({ops.n_g} cells) "
+                   f"{args.scheme} dt={spec.dt} tol={spec.tol}", "cells": ops.n_g},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{nsteps} {args.scheme} step(s) of {args.config} from "
+                                   "the seeded initial state (cold engine seeds); "
+                                   "scipy csr_matvec is single-threaded, BLAS uses all "
+                                   "cores"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import torch
+    from paper_1805_02144_b200 import swe as gswe
+    from paper_1805_02144_b200.states import make_config
+
+    ops, u0, spec = make_config(args.config)
+    scheme = args.scheme
+    ctx = gswe.SweContext(ops, device=local)
+    ctx.set_state(u0)
+    ctx.reset_seeds()
+    first = True
+
+    def step():
+        nonlocal first
+        sch = "rb_euler" if (scheme == "epi3" and first) else scheme
+        first = False
+        return ctx.step(sch, spec.dt, spec.tol)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(local)
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    l0 = ctx.launches()
+    k0 = ctx.krylov_iters()
+    dev_ms = 0.0
+    mv = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        calls = step()
+        dev_ms += ctx.last_kernel_ms()
+        mv += sum(int(c.matvecs) for c in calls)
+    torch.cuda.synchronize(local)
+    wall = time.perf_counter() - t0
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    launches = ctx.launches() - l0
+    kiters = ctx.krylov_iters() - k0
+    ms = dev_ms
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+
+    # end to end through the C ABI: pinned host state in, step, state out
+    pin_in = torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory()
+    pin_out = torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory()
+    hin, hout = pin_in.numpy(), pin_out.numpy()
+    hin[:] = ctx.get_state()
+    torch.cuda.synchronize(local)
+    te = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        ctx.set_state(hin)
+        step()
+        from paper_1805_02144_b200 import _native as nat
+        nat.check(nat.load().eik_swe_get_state(ctx.h, nat.dptr(hout)), "get_state")
+        hin[:] = hout
+    e2e_wall = time.perf_counter() - te
+    e2e = ws * args.e2e_steps / e2e_wall
+    if dist:
+        t = torch.tensor([e2e_wall], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = ws * args.e2e_steps / float(t.item())
+
+    hbm, src = peaks()
+    balg = b_alg_per_iter(ops)
+    it_per_step = kiters / args.steps
+    achieved = balg * kiters / (dev_ms / 1e3) / 1e9
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE C3 jet state on our icosahedral grid)",
+        "config": {"workload": f"{args.config}: L{ops.level} icosahedral ({ops.n_g} cells) "
+                   f"{scheme} dt={spec.dt}s tol={spec.tol}",
+                   "cells": ops.n_g, "parallelism": f"replicas x{ws}",
+                   "l2": "no flush: inputs > L2 (each Krylov iteration streams ~0.5 GB)"},
+        "krylov_iters_per_step": it_per_step, "matvecs_per_step": mv / args.steps,
+        "wall_ms_per_step": 1e3 * wall / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None,
+                     "note": f"kernel = whole-step k_swe_step; achieved = B_alg "
+                             f"({balg / 1e6:.1f} MB/iter, SURVEY §8d) x Krylov iters / "
+                             f"step-kernel time; peak {src}"},
+        "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * 4 * ops.n_g,
+                "d2h_bytes_per_step": 8 * 4 * ops.n_g},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        spec.scheme = scheme
+        secs = cpu_baseline_oracle(ops, u0, spec, 1)
+        line["cpu_baseline"] = {
+            "value": 1.0 / secs, "unit": "steps/s", "cores": threads, "kind": "port",
+            "sample": f"1 {scheme} step of {args.config} from the initial state (oracle "
+                      "port, cold seeds); scipy csr_matvec single-threaded"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
