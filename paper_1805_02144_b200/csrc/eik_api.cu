@@ -213,7 +213,7 @@ __device__ EngineTask base_task(const SweArgs& A) {
 
 // ---------------------------------------------------------------- step kernel
 // One whole integrator step (integrators.py:140-224) on the resident state.
-__global__ void __launch_bounds__(TPB) k_swe_step(SweArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_swe_step(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(TPB) k_swe_step(SweArgs A) {
 }
 
 // ------------------------------------------------------- API-level kernels
-__global__ void __launch_bounds__(TPB) k_swe_rhs(SweArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_swe_rhs(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(TPB) k_swe_rhs(SweArgs A) {
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB) k_swe_jv(SweArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_swe_jv(SweArgs A) {
   // A.x = linearisation state, A.va = direction, A.out = J v
   __shared__ Smem sm;
   smem_init(sm);
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(TPB) k_swe_jv(SweArgs A) {
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB) k_swe_nnz(SweArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_swe_nnz(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(TPB) k_swe_nnz(SweArgs A) {
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB) k_swe_phipm(SweArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_swe_phipm(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
@@ -422,7 +422,7 @@ struct CsrArgs {
   int* status;
 };
 
-__global__ void __launch_bounds__(TPB) k_csr_phipm(CsrArgs A) {
+__global__ void __launch_bounds__(TPB, 1) k_csr_phipm(CsrArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
@@ -456,15 +456,16 @@ struct Bufs {
   }
 };
 
-int coop_grid(const void* const* kernels, int nk, int dev, int64_t NU) {
+int coop_grid(const void* const* kernels, int nk, int dev, int64_t NU, size_t smem) {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int best = 1 << 30;
   for (int k = 0; k < nk; ++k) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernels[k], TPB, 0);
-    best = std::min(best, std::max(nb, 1) * nsm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernels[k], TPB, smem);
+    best = std::min(best, nb * nsm);
   }
+  if (best < 1) return 0;
   const int64_t need = (NU + TPB - 1) / TPB;
   return (int)std::max<int64_t>(1, std::min<int64_t>(best, need));
 }
@@ -489,17 +490,29 @@ struct EngineHost {
   unsigned long long* kiters_d = nullptr;
   int64_t launches = 0;
 
+  size_t smem = 0;
   eik_status init(int device, int64_t NU_, int64_t n_, int64_t m_alloc_,
-                  const void* const* kernels, int nk) {
+                  const void* const* kernels, int nk, size_t smem_bytes = 0,
+                  int G_override = 0) {
     dev = device;
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     NU = NU_;
     n = n_;
     m_alloc = std::max<int64_t>(1, m_alloc_);
-    G = coop_grid(kernels, nk, dev, NU);
+    smem = smem_bytes;
+    for (int k = 0; k < nk; ++k)
+      CK(cudaFuncSetAttribute(kernels[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(smem, 1)));
+    G = coop_grid(kernels, nk, dev, NU, smem);
+    if (G_override > 0) {
+      if (G_override > G)
+        return fail(EIK_ECUDA, "cooperative grid does not fit the device");
+      G = G_override;
+    }
     CK(mem.get(&wk.basis, (size_t)m_alloc * NU));
     CK(mem.get(&wk.zbuf, NU));
+    CK(mem.get(&wk.zbuf2, NU));
     for (int l = 1; l < MAXV; ++l) CK(mem.get(&wk.w[l], NU));
     CK(mem.get(&wk.ybuf[0], NU));
     CK(mem.get(&wk.ybuf[1], NU));
@@ -513,7 +526,7 @@ struct EngineHost {
     CK(mem.get(&trace_len_d, 1));
     CK(mem.get(&status_d, 1));
     CK(mem.get(&nnz_d, 1));
-    CK(mem.get(&kiters_d, 1));
+    CK(mem.get(&kiters_d, 4));
     wk.info = info_d;
     wk.trace = nullptr;
     wk.trace_cap = 0;
@@ -659,7 +672,7 @@ struct EikSwe {
   }
   eik_status launch(const void* fn_, SweArgs& A) {
     void* kargs[] = {&A};
-    CK(cudaLaunchCooperativeKernel(fn_, eng.G, TPB, kargs, 0, eng.st));
+    CK(cudaLaunchCooperativeKernel(fn_, eng.G, TPB, kargs, eng.smem, eng.st));
     ++eng.launches;
     return EIK_OK;
   }
@@ -769,12 +782,67 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
         else if (Df.data[k] != 0.0) dfx[i] += 1;
       }
   }
+  // ---- tiles along the Hilbert order, one CTA per SM, each tile <= TPB own
+  // cells plus its 2-ring halo (local indices into shared memory)
+  int nsm = 0;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return fail(EIK_ECUDA, "no CUDA device");
+  const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (N + TPB - 1) / TPB));
+  const int64_t per = (N + (int64_t)Gt * TPB - 1) / ((int64_t)Gt * TPB);
+  const int NT = (int)(Gt * per);
+  const int64_t tsz = (N + NT - 1) / NT;
+  std::vector<int32_t> t_cell0(NT), t_nT(NT), t_nE1(NT), t_nE2(NT), t_e2off(NT), t_e1off(NT);
+  std::vector<int32_t> e2map;
+  std::vector<int16_t> lnbr;
+  int e1max = 1, e2max = 1;
+  {
+    std::vector<int32_t> loc(N, -1), list;
+    for (int t = 0; t < NT; ++t) {
+      const int64_t lo = std::min<int64_t>(N, t * tsz), hi = std::min<int64_t>(N, lo + tsz);
+      list.clear();
+      for (int64_t i = lo; i < hi; ++i) { loc[i] = (int32_t)list.size(); list.push_back((int32_t)i); }
+      const int nT = (int)list.size();
+      for (int64_t i = lo; i < hi; ++i)
+        for (int q = 0; q < cnt[i]; ++q) {
+          const int32_t j = nbr[(size_t)q * N + i];
+          if (loc[j] < 0) { loc[j] = (int32_t)list.size(); list.push_back(j); }
+        }
+      const int nE1 = (int)list.size();
+      for (int c2 = nT; c2 < nE1; ++c2) {
+        const int32_t gi = list[c2];
+        for (int q = 0; q < cnt[gi]; ++q) {
+          const int32_t j = nbr[(size_t)q * N + gi];
+          if (loc[j] < 0) { loc[j] = (int32_t)list.size(); list.push_back(j); }
+        }
+      }
+      const int nE2 = (int)list.size();
+      if (nE2 > 32767) return fail(EIK_EINVAL, "tile halo too large");
+      t_cell0[t] = (int32_t)lo; t_nT[t] = nT; t_nE1[t] = nE1; t_nE2[t] = nE2;
+      t_e2off[t] = (int32_t)e2map.size();
+      t_e1off[t] = (int32_t)(lnbr.size() / 8);
+      for (int c2 = 0; c2 < nE1; ++c2) {
+        const int32_t gi = list[c2];
+        for (int q = 0; q < 8; ++q) {
+          const int32_t j = q < K ? nbr[(size_t)q * N + gi] : gi;
+          lnbr.push_back((int16_t)loc[j]);
+        }
+      }
+      for (int32_t g2 : list) { e2map.push_back(g2); loc[g2] = -1; }
+      e1max = std::max(e1max, nE1);
+      e2max = std::max(e2max, nE2);
+    }
+  }
+  std::vector<double> Lc((size_t)N * 8, 0.0);
+  for (int64_t i = 0; i < N; ++i)
+    for (int q = 0; q < K; ++q) Lc[(size_t)i * 8 + q] = coef[((size_t)q * NOPS + OP_L) * N + i];
+
   EikSwe* c = new EikSwe();
   c->N = N;
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
   eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
-                             kSweKernels, 5);
+                             kSweKernels, 5, tile_smem_bytes(e1max, e2max), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
   int *d_nbr, *d_dfx, *d_cnt;
@@ -802,6 +870,27 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(cudaMemcpy(d_dfx, dfx.data(), dfx.size() * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_cnt, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_hs, h_s, N * 8, cudaMemcpyHostToDevice));
+  int *d_tc0, *d_tnT, *d_tnE1, *d_tnE2, *d_te2, *d_te1, *d_e2map;
+  short* d_lnbr;
+  double* d_Lc;
+  CKC(B.get(&d_tc0, NT));
+  CKC(B.get(&d_tnT, NT));
+  CKC(B.get(&d_tnE1, NT));
+  CKC(B.get(&d_tnE2, NT));
+  CKC(B.get(&d_te2, NT));
+  CKC(B.get(&d_te1, NT));
+  CKC(B.get(&d_e2map, e2map.size()));
+  CKC(B.get(&d_lnbr, lnbr.size()));
+  CKC(B.get(&d_Lc, Lc.size()));
+  CKC(cudaMemcpy(d_tc0, t_cell0.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnT, t_nT.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnE1, t_nE1.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnE2, t_nE2.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_te2, t_e2off.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_te1, t_e1off.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_e2map, e2map.data(), e2map.size() * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_lnbr, lnbr.data(), lnbr.size() * 2, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_Lc, Lc.data(), Lc.size() * 8, cudaMemcpyHostToDevice));
   {
     std::vector<double4> nf(N);
     for (int64_t i = 0; i < N; ++i) nf[i] = make_double4(n_x[i], n_y[i], n_z[i], f[i]);
@@ -843,6 +932,18 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.df1 = d_df1;
   S.dfx = d_dfx;
   S.cnt = d_cnt;
+  S.ntiles = NT;
+  S.t_cell0 = d_tc0;
+  S.t_nT = d_tnT;
+  S.t_nE1 = d_tnE1;
+  S.t_nE2 = d_tnE2;
+  S.t_e2off = d_te2;
+  S.t_e1off = d_te1;
+  S.e2map = d_e2map;
+  S.lnbr = d_lnbr;
+  S.Lc = d_Lc;
+  S.e1max = e1max;
+  S.e2max = e2max;
   *out = c;
   return EIK_OK;
 }
@@ -982,8 +1083,8 @@ static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol)
       bool ok = cudaStreamBeginCapture(c->eng.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
       if (ok) {
         void* kargs[] = {&A};
-        ok = cudaLaunchCooperativeKernel((const void*)k_swe_step, c->eng.G, TPB, kargs, 0,
-                                         c->eng.st) == cudaSuccess;
+        ok = cudaLaunchCooperativeKernel((const void*)k_swe_step, c->eng.G, TPB, kargs,
+                                         c->eng.smem, c->eng.st) == cudaSuccess;
         ok = (cudaStreamEndCapture(c->eng.st, &graph) == cudaSuccess) && ok;
       }
       if (ok) ok = cudaGraphInstantiate(&c->gexec, graph, 0) == cudaSuccess;
@@ -1158,7 +1259,7 @@ eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
   A.status = E.status_d;
   CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
   void* kargs[] = {&A};
-  CK(cudaLaunchCooperativeKernel((const void*)k_csr_phipm, E.G, TPB, kargs, 0, E.st));
+  CK(cudaLaunchCooperativeKernel((const void*)k_csr_phipm, E.G, TPB, kargs, E.smem, E.st));
   ++E.launches;
   s = E.finish_phipm(info, trace, trace_cap, trace_len);
   if (s != EIK_OK) return s;

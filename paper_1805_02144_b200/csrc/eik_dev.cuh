@@ -25,14 +25,18 @@ namespace cg = cooperative_groups;
 
 namespace eik {
 
-constexpr int TPB = 256;
+constexpr int TPB = 512;        // one CTA of 16 warps per SM (<=128 regs)
 constexpr int NWARP = TPB / 32;
 constexpr int NPART = 8;   // doubles per CTA partial record
 constexpr int MAXV = 8;    // v_0..v_7
 constexpr int MAXNS = 8;   // output points
 constexpr int MAXDIM = kDenseCap;
 constexpr int KMAX = 8;    // stencil slots per cell (self + up to 7)
-constexpr int NOPS = 10;   // Gx Gy Gz Dx Dy Dz Vx Vy Vz L
+constexpr int NOPS = 10;
+// Gram-identity norm of the orthogonalised vector is used while it keeps
+// h^2 > kGramSafe ||z||^2 (relative error of h below ~1e-14); else an
+// explicit orthogonalisation pass recomputes it.
+constexpr double kGramSafe = 1e-2;   // Gx Gy Gz Dx Dy Dz Vx Vy Vz L
 enum { OP_GX = 0, OP_GY, OP_GZ, OP_DX, OP_DY, OP_DZ, OP_VX, OP_VY, OP_VZ, OP_L };
 
 // ------------------------------------------------------------ double4 math
@@ -168,7 +172,21 @@ struct SweOp {
   const double* df1;     // [K][N] Df(i, slot) (0 where Df has no entry)
   const int* dfx;        // [N] nonzero Df entries outside the slot set
   const int* cnt;        // [N] valid slots
+  // tiled single-pass Krylov iteration (cells tiled along the Hilbert order;
+  // each tile's 2-ring halo is staged in shared memory)
+  int ntiles;
+  const int* t_cell0;    // first own cell
+  const int* t_nT;       // own cells (<= TPB)
+  const int* t_nE1;      // own + 1-ring halo
+  const int* t_nE2;      // own + 1-ring + 2-ring halo
+  const int* t_e2off;    // offset into e2map
+  const int* t_e1off;    // offset into lnbr (rows)
+  const int* e2map;      // local -> global cell id, order [own, H1, H2]
+  const short* lnbr;     // [rows][8] local neighbour slots of E1 cells
+  const double* Lc;      // [N][8] Laplacian row in slot order (cell-major)
+  int e1max, e2max;
 
+  static constexpr bool kTiled = true;
   __device__ __forceinline__ int64_t NU() const { return N; }
   __device__ __forceinline__ double c(int s, int op, int64_t i) const {
     return __ldg(coef + ((int64_t)s * NOPS + op) * N + i);
@@ -280,6 +298,139 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
   return r;
 }
 
+
+// ------------------------------------------------------------ tiled pass
+// Dynamic shared memory of one CTA: the tile's vector on E2, its Laplacian
+// and the linearisation state on E1, the E2 local->global map.
+struct TileSmem {
+  double4* x;
+  double4* La;
+  double4* U;
+  int* gid;
+};
+
+__device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  TileSmem t;
+  t.x = reinterpret_cast<double4*>(dsm);
+  t.La = t.x + S.e2max;
+  t.U = t.La + S.e1max;
+  t.gid = reinterpret_cast<int*>(t.U + S.e1max);
+  return t;
+}
+
+__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
+  return (size_t)e2max * 32 + (size_t)e1max * 64 + (size_t)e2max * 4 + 16;
+}
+
+struct Row8 {
+  short s[8];
+};
+__device__ __forceinline__ Row8 load_row8(const short* p) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(p));
+  Row8 r;
+  memcpy(&r, &v, 16);
+  return r;
+}
+
+// J x for own cell `c` of the tile (x, La, U staged in smem)
+__device__ __forceinline__ double4 swe_jv_tile(const SweOp& S, const TileSmem& ts,
+                                               const Row8& row, int c, int64_t i) {
+  double zeta = 0.0, gx = 0.0, gy = 0.0, gz = 0.0, dv = 0.0;
+  double4 ll = d4(0.0);
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    if (s < S.K) {
+      const int l = row.s[s];
+      const double4 aj = ts.x[l];
+      const double4 U = ts.U[l];
+      const double4 la = ts.La[l];
+      const double* cp = S.coef + (int64_t)s * NOPS * S.N + i;
+      const double vx = __ldcs(cp + OP_VX * S.N), vy = __ldcs(cp + OP_VY * S.N),
+                   vz = __ldcs(cp + OP_VZ * S.N);
+      const double gcx = __ldcs(cp + OP_GX * S.N), gcy = __ldcs(cp + OP_GY * S.N),
+                   gcz = __ldcs(cp + OP_GZ * S.N);
+      const double dx = __ldcs(cp + OP_DX * S.N), dy = __ldcs(cp + OP_DY * S.N),
+                   dz = __ldcs(cp + OP_DZ * S.N);
+      const double l0 = __ldcs(cp + OP_L * S.N);
+      zeta += vx * aj.x + vy * aj.y + vz * aj.z;
+      const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
+      gx += gcx * e;
+      gy += gcy * e;
+      gz += gcz * e;
+      dv += dx * (U.w * aj.x + U.x * aj.w) + dy * (U.w * aj.y + U.y * aj.w) +
+            dz * (U.w * aj.z + U.z * aj.w);
+      ll.x += l0 * la.x;
+      ll.y += l0 * la.y;
+      ll.z += l0 * la.z;
+      ll.w += l0 * la.w;
+    }
+  }
+  const double4 ai = ts.x[c];
+  const double4 U = ts.U[c];
+  const double4 q = S.ne[i];
+  const double px = q.y * U.z - q.z * U.y;
+  const double py = q.z * U.x - q.x * U.z;
+  const double pz = q.x * U.y - q.y * U.x;
+  const double cx = q.y * ai.z - q.z * ai.y;
+  const double cy = q.z * ai.x - q.x * ai.z;
+  const double cz = q.x * ai.y - q.y * ai.x;
+  double4 r;
+  r.x = -(px * zeta) - q.w * cx - gx - S.nu * ll.x;
+  r.y = -(py * zeta) - q.w * cy - gy - S.nu * ll.y;
+  r.z = -(pz * zeta) - q.w * cz - gz - S.nu * ll.z;
+  r.w = -dv - S.nu * ll.w;
+  return r;
+}
+
+// One pass over every tile: x = form(g, own) on E2 -> smem, L x on E1,
+// z = scale * J x on the own cells -> epi(i, c, z, x_i).  A whole Krylov
+// iteration (orthogonalise + normalise v_j, L v_j, J v_j, projections) is
+// one such pass: one HBM sweep and one grid barrier per iteration.
+template <class Form, class Epi>
+__device__ void swe_tiled(const SweOp& S, const Form& form, const Epi& epi) {
+  const TileSmem ts = tile_smem(S);
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+    const int64_t c0 = __ldg(S.t_cell0 + t);
+    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+    const int* map = S.e2map + __ldg(S.t_e2off + t);
+    const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+    for (int c = threadIdx.x; c < nE2; c += TPB) {
+      const int g = __ldg(map + c);
+      ts.gid[c] = g;
+      ts.x[c] = form(g, c < nT);
+      if (c < nE1) ts.U[c] = S.lin[g];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nE1; c += TPB) {
+      const Row8 row = load_row8(rows + (int64_t)c * 8);
+      const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
+      double4 acc = d4(0.0);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (s < S.K) {
+          const double l = __ldg(lc + s);
+          const double4 xv = ts.x[row.s[s]];
+          acc.x += l * xv.x;
+          acc.y += l * xv.y;
+          acc.z += l * xv.z;
+          acc.w += l * xv.w;
+        }
+      }
+      ts.La[c] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < nT) {
+      const int c = threadIdx.x;
+      const int64_t i = c0 + c;
+      const Row8 row = load_row8(rows + (int64_t)c * 8);
+      const double4 z = S.scale * swe_jv_tile(S, ts, row, c, i);
+      epi(i, z, ts.x[c]);
+    }
+    __syncthreads();
+  }
+}
+
 struct SrcPtr {
   const double4* p;
   __device__ __forceinline__ double4 operator()(int64_t j) const { return p[j]; }
@@ -292,6 +443,7 @@ struct SrcDiff {  // a[j] - b[j]
 
 // Generic CSR operator on a zero-padded plain vector (units of 4 rows).
 struct CsrOp {
+  static constexpr bool kTiled = false;
   int64_t n, NUu;
   const int* rp;
   const int* ci;
@@ -516,6 +668,7 @@ struct EngineTask {
 struct EngineWork {
   double4* basis;           // m_alloc * NU
   double4* zbuf;            // raw next Krylov vector
+  double4* zbuf2;           // second z buffer (tiled path ping-pong)
   double4* w[MAXV];         // w_1..w_p
   double4* ybuf[2];
   double4* zero;            // an all-zero vector (y when v_0 == 0)
@@ -624,20 +777,38 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         double cl[MAXV];
         for (int ell = 0; ell <= p - j; ++ell) cl[ell] = pow_over_fact(t, ell);
         const bool do_mv = !(T.zero_skip && !wprev_nz);
-        if (do_mv) {
-          op_pre(op, wprev, 1.0, lo, hi);
-          grid.sync();
-          ++mv;
-        }
         double4* wj = Wk.w[j];
         double r[2] = {0.0, 0.0};
-        for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-          double4 a = do_mv ? op_main(op, wprev, u) : d4(0.0);
-          for (int ell = 0; ell <= p - j; ++ell)
-            if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][u];
-          wj[u] = a;
-          r[0] += nz4(a);
-          r[1] += dot4(a, a);
+        if constexpr (Op::kTiled) {
+          if (do_mv) {
+            ++mv;
+            const double4* src = wprev;
+            swe_tiled(op, [&](int64_t g, bool) { return src[g]; },
+                      [&](int64_t i, double4 z, double4) {
+                        double4 a = z;
+                        for (int ell = 0; ell <= p - j; ++ell)
+                          if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][i];
+                        wj[i] = a;
+                        r[0] += nz4(a);
+                        r[1] += dot4(a, a);
+                      });
+          }
+        } else {
+          if (do_mv) {
+            op_pre(op, wprev, 1.0, lo, hi);
+            grid.sync();
+            ++mv;
+          }
+        }
+        if (!Op::kTiled || !do_mv) {
+          for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+            double4 a = do_mv ? op_main(op, wprev, u) : d4(0.0);
+            for (int ell = 0; ell <= p - j; ++ell)
+              if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][u];
+            wj[u] = a;
+            r[0] += nz4(a);
+            r[1] += dot4(a, a);
+          }
         }
         grid_reduce<2>(grid, sm, r, Wk.part);
         wprev = wj;
@@ -662,6 +833,12 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
       double beta = 0.0, hnext = 0.0, eps = 0.0, nh = 0.0, corner = 0.0;
       bool broke = false;
       int64_t keep = 0;
+      // v_{m+1} = ((z - h1 v_{m-1}) - h2 v_m) / h_next (tiled path) or z / h_next
+      const double4* vnext_z = Wk.zbuf;
+      const double4* vnext_m1 = nullptr;
+      const double4* vnext_v = nullptr;
+      double vnext_h1 = 0.0, vnext_h2 = 0.0;
+      bool vnext_expl = true;
       if (wp_nz) {
         beta = sqrt(ssq);
         const int64_t m_eff = m < n ? m : n;
@@ -673,7 +850,98 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         double hcur = beta;
         const double4* raw = wp;
         keep = m_eff;
-        for (int64_t j = 0; j < m_eff; ++j) {
+        bool tiled_done = false;
+        if constexpr (Op::kTiled) {
+          if (iom == 2) {
+            tiled_done = true;
+            // one tiled pass + one grid barrier per iteration: v_j is formed
+            // on the fly from (z_{j-1}, v_{j-2}, v_{j-1}) with the previous
+            // iteration's MGS coefficients, its norm taken from the Gram
+            // identity (explicit pass only when that would cancel)
+            double h1 = 0.0, h2 = 0.0, nm1 = 0.0;
+            bool expl = false;
+            for (int64_t j = 0; j < m_eff; ++j) {
+              double4* vj = Wk.basis + j * NU;
+              const double4* vm1 = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
+              const double4* vm2 = j > 1 ? Wk.basis + (j - 2) * NU : nullptr;
+              const double4* zin = (j & 1) ? Wk.zbuf : Wk.zbuf2;
+              double4* zout = (j & 1) ? Wk.zbuf2 : Wk.zbuf;
+              double d[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+              const double hc = hcur, a1 = h1, a2 = h2;
+              const int mode = j == 0 ? 0 : (expl ? 0 : (vm2 ? 2 : 1));
+              const double4* src = j == 0 ? wp : zin;
+              swe_tiled(
+                  op,
+                  [&](int64_t g, bool own) {
+                    double4 x = src[g];
+                    if (mode == 2) x = x - a1 * vm2[g];
+                    if (mode >= 1) x = x - a2 * vm1[g];
+                    x = div4(x, hc);
+                    if (own) vj[g] = x;
+                    return x;
+                  },
+                  [&](int64_t i, double4 z, double4 x) {
+                    zout[i] = z;
+                    d[1] += dot4(x, z);
+                    d[3] += dot4(z, z);
+                    d[4] += dot4(x, x);
+                    if (vm1) {
+                      const double4 b = vm1[i];
+                      d[0] += dot4(b, z);
+                      d[2] += dot4(x, b);
+                    }
+                  });
+              ++mv;
+              if (lead) atomicAdd(Wk.kiters, 1ull);
+              grid_reduce<5>(grid, sm, d, Wk.part);
+              const double h1n = vm1 ? d[0] : 0.0;
+              const double h2n = vm1 ? d[1] - h1n * d[2] : d[1];
+              if (lead) {
+                if (vm1) Wk.H[(j - 1) * ld + j] = h1n;
+                Wk.H[j * ld + j] = h2n;
+              }
+              double hsq = d[3] - 2.0 * h2n * d[1] + h2n * h2n * d[4];
+              if (vm1) hsq += -2.0 * h1n * d[0] + h1n * h1n * nm1 + 2.0 * h1n * h2n * d[2];
+              expl = !(hsq > kGramSafe * d[3]);
+              if (expl) {
+                double r[1] = {0.0};
+                for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+                  double4 z = zout[u];
+                  if (vm1) z = z - h1n * vm1[u];
+                  z = z - h2n * vj[u];
+                  zout[u] = z;
+                  r[0] += dot4(z, z);
+                }
+                grid_reduce<1>(grid, sm, r, Wk.part);
+                hsq = r[0];
+                if (lead) atomicAdd(Wk.kiters + 1, 1ull);
+              }
+              const double h = sqrt(hsq);
+              nm1 = d[4];
+              if (h < kBreakdownTol * beta) {
+                broke = true;
+                keep = j + 1;
+                hnext = 0.0;
+                break;
+              }
+              if (j + 1 < m_eff) {
+                if (lead) Wk.H[(j + 1) * ld + j] = h;
+                hcur = h;
+                h1 = h1n;
+                h2 = h2n;
+              } else {
+                hnext = h;
+                vnext_z = zout;
+                vnext_h1 = h1n;
+                vnext_h2 = h2n;
+                vnext_m1 = vm1;
+                vnext_v = vj;
+                vnext_expl = expl;
+              }
+            }
+          }
+        }
+        for (int64_t j = 0; j < m_eff && !tiled_done; ++j) {
           double4* vj = Wk.basis + j * NU;
           const double4* vjm = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
           // v_j = raw / h (exact division), La = L v_j
@@ -814,7 +1082,14 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
             double4 s = d4(0.0);
             for (int64_t k = 0; k < keep; ++k) s = s + sm.phi[k] * Wk.basis[k * NU + u];
             double4 ap = beta * s;
-            if (!broke) ap = ap + corr * div4(Wk.zbuf[u], hnext);
+            if (!broke) {
+              double4 zz = vnext_z[u];
+              if (!vnext_expl) {
+                if (vnext_m1) zz = zz - vnext_h1 * vnext_m1[u];
+                zz = zz - vnext_h2 * vnext_v[u];
+              }
+              ap = ap + corr * div4(zz, hnext);
+            }
             c = c + tp * ap;
           }
           cand[u] = c;
