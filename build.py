@@ -25,10 +25,10 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, out=OUT, defines=()):
+    if not force and out == OUT and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *SRC]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp", *SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(ROOT, "build", "ptxas.log")
     os.makedirs(os.path.dirname(log), exist_ok=True)
@@ -37,11 +37,18 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libeik.so")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
         print(r.stderr)
     return OUT
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--variant" in sys.argv:
+        # python build.py --variant NAME DEF1 DEF2 ...  -> build/libeik_NAME.so
+        k = sys.argv.index("--variant")
+        name, defs = sys.argv[k + 1], sys.argv[k + 2:]
+        print(build(force=True, out=os.path.join(ROOT, "build", f"libeik_{name}.so"),
+                    defines=defs))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

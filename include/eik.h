@@ -150,6 +150,20 @@ eik_status eik_swe_seeds(EikSwe* ctx, int32_t slot, double* tau, int64_t* m,
                          int32_t set);
 eik_status eik_swe_reset_seeds(EikSwe* ctx);
 
+/* Krylov microbenchmark: reps IOM2 sweeps of dimension m (A = dt J(u)) on
+ * direction v, device time of the whole launch in out[0] (ms), kept
+ * dimension in out[1] */
+eik_status eik_swe_krylov_bench(EikSwe* ctx, const double* u, const double* v,
+                                double dt, int32_t m, int32_t reps, double* out);
+/* out[9]: grid CTAs, threads/CTA, tiles, max E1, max E2, slots, compact
+ * slots, compact stencil valid, dynamic smem bytes */
+eik_status eik_swe_info(const EikSwe* ctx, int64_t* out);
+
+/* EIK_PROF builds: per-phase clock64 totals of CTA 0 (16 doubles: rhs, nnz,
+ * w-recurrence, Krylov, dense exp, candidate, stage perturbation, misc);
+ * returns EIK_EINVAL in normal builds */
+int eik_prof_read(double* out, int reset);
+
 /* launches of libeik kernels since creation (for bench gpu_launches) */
 int64_t eik_swe_launches(const EikSwe* ctx);
 /* last step's per-phase device time in ms (CUDA events), engine-kernel only */

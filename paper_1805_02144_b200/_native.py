@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeik.so")
+LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(_HERE, "libeik.so")
 
 EIK_OK, EIK_EINVAL, EIK_ENONFINITE, EIK_EPHIPM, EIK_ECUDA, EIK_ENOMEM = range(6)
 SCHEME_IDS = {"rb_euler": 0, "epi3": 1, "exprb42": 2, "pexprb43": 3,
@@ -77,6 +77,9 @@ _SIGS = {
     "eik_swe_seeds": (C.c_int, [_P, C.c_int32, _D, C.POINTER(C.c_int64),
                                 C.c_int32]),
     "eik_swe_reset_seeds": (C.c_int, [_P]),
+    "eik_swe_krylov_bench": (C.c_int, [_P, _D, _D, C.c_double, C.c_int32, C.c_int32, _D]),
+    "eik_swe_info": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "eik_prof_read": (C.c_int, [_D, C.c_int]),
     "eik_swe_launches": (C.c_int64, [_P]),
     "eik_swe_last_kernel_ms": (C.c_double, [_P]),
     "eik_swe_krylov_iters": (C.c_int64, [_P]),

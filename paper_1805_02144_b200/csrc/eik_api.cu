@@ -18,6 +18,9 @@ using namespace eik;
 
 // ====================================================================== errors
 static thread_local std::string g_err;
+// dynamic smem floor: the dense phase keeps its 6 matrices in shared memory
+// for n = m + p + 1 <= 46
+static constexpr size_t kDenseSmemBytes = 128 + (size_t)6 * 46 * 46 * 8;
 static eik_status fail(eik_status s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -32,7 +35,11 @@ static eik_status fail(eik_status s, const std::string& msg) {
 // ====================================================================== kernels
 
 __device__ __forceinline__ void smem_init(Smem& sm) {
-  if (threadIdx.x == 0) sm.par = 0;
+  if (threadIdx.x == 0) {
+    sm.par = 0;
+    sm.bar_init = 0;
+    sm.tphase = 0;
+  }
   __syncthreads();
 }
 
@@ -54,7 +61,8 @@ __global__ void k_cell_to_soa(const double4* __restrict__ d, double* s, int64_t 
 }
 
 struct SweArgs {
-  SweOp S;
+  SweOp S1;   // J at the linearisation state (scale 1)
+  SweOp SD;   // dt * J (the engine operator, integrators.py:117)
   EngineWork Wk;
   // step buffers
   double4 *u, *uprev, *fn, *v1, *va, *vb, *d2, *Ub, *W[5];
@@ -91,6 +99,7 @@ __device__ int phase_rhs(cg::grid_group& grid, Smem& sm, const SweOp& S,
     if (out_v) out_v[i] = dt * F;
     r[0] += nf4(F) + nf4(w[i]);
   }
+  if (write_eta) fence_proxy_async_global();  // ne is read by TMA later
   grid_reduce<1>(grid, sm, r, part);
   return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
 }
@@ -213,144 +222,135 @@ __device__ EngineTask base_task(const SweArgs& A) {
 
 // ---------------------------------------------------------------- step kernel
 // One whole integrator step (integrators.py:140-224) on the resident state.
-__global__ void __launch_bounds__(TPB, 1) k_swe_step(SweArgs A) {
+// The engine is invoked from a single call site (a loop over the scheme's
+// 1-3 engine calls) so that one inlined copy of it exists and the operator
+// structs stay in kernel-parameter space (A.S1: J, A.SD: dt*J, lin = u_n).
+__global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  SweOp S = A.S;
-  S.lin = A.u;
-  EngineWork Wk = A.Wk;
   const double dt = A.dt;
-  int st = phase_rhs(grid, sm, S, A.u, A.fn, A.v1, dt, true, Wk.part);
+  const int scheme = A.scheme;
+  ProfClock pc;
+  int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, dt, true, A.Wk.part);
+  pc.mark(PC_RHS);
   if (st != EIK_OK) { set_status(A.status, st); return; }
-  Wk.nnz = (int64_t)phase_count_nnz(grid, sm, S, Wk.part);
-  SweOp SA = S;
-  SA.scale = dt;
+  const int64_t nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);
+  pc.mark(PC_NNZ);
+  const int ncalls = scheme == EIK_EXPRB53 ? 3 : (scheme >= EIK_EXPRB42 ? 2 : 1);
   const double4* u = A.u;
   double4* Ub = A.Ub;
   double4 *va = A.va, *vb = A.vb, *d2 = A.d2;
-  EngineTask T = base_task(A);
-  double4* fin = nullptr;      // W column added in the final combination
-  const double4* base = u;     // u_{n+1} = base + fin
-  switch (A.scheme) {
-    case EIK_RB_EULER: {
-      T.p = 1; T.v[1] = A.v1; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[0];
-      T.slot = EIK_SLOT_RBE; T.info_idx = 0;
-      st = engine_call(grid, sm, SA, T, Wk);
-      fin = A.W[0];
-      break;
-    }
-    case EIK_EPI3: {
+  double4* const* W = A.W;
+  const double4* base = u;  // u_{n+1} = base + fin
+  const double4* fin = nullptr;
+  for (int call = 0; call < ncalls && st == EIK_OK; ++call) {
+    // ---- stage work before the engine call; task of this call
+    EngineTask T = base_task(A);
+    T.info_idx = call;
+    T.ns = 1;
+    T.rho[0] = 1.0;
+    const int key = scheme * 4 + call;
+    if (key == EIK_EPI3 * 4) {
       const double c = (2.0 / 3.0) * dt;
-      st = phase_dev(grid, sm, S, A.uprev, A.fn,
-                     [&](int64_t i, double4 d) { va[i] = c * d; }, Wk.part);
-      if (st != EIK_OK) break;
-      T.p = 2; T.v[1] = A.v1; T.v[2] = va; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[0];
-      T.slot = EIK_SLOT_EPI3; T.info_idx = 0;
-      st = engine_call(grid, sm, SA, T, Wk);
-      fin = A.W[0];
-      break;
-    }
-    case EIK_EXPRB42: {
-      T.p = 1; T.v[1] = A.v1; T.ns = 1; T.rho[0] = 0.75; T.W[0] = A.W[0];
-      T.slot = EIK_SLOT_EXPRB42_1; T.info_idx = 0;
-      st = engine_call(grid, sm, SA, T, Wk);
-      if (st != EIK_OK) break;
-      double4* W0 = A.W[0];
-      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
+      st = phase_dev(grid, sm, A.S1, A.uprev, A.fn,
+                     [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
+    } else if (key == EIK_EXPRB42 * 4 + 1) {
+      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
       grid.sync();
       const double c = (32.0 / 9.0) * dt;
-      st = phase_dev(grid, sm, S, Ub, A.fn,
-                     [&](int64_t i, double4 d) { va[i] = c * d; }, Wk.part);
-      if (st != EIK_OK) break;
-      T = base_task(A);
-      T.p = 3; T.v[1] = A.v1; T.v[3] = va; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[1];
-      T.slot = EIK_SLOT_EXPRB42_2; T.info_idx = 1;
-      st = engine_call(grid, sm, SA, T, Wk);
-      fin = A.W[1];
-      break;
-    }
-    case EIK_PEXPRB43: {
-      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 1.0;
-      T.W[0] = A.W[0]; T.W[1] = A.W[1];
-      T.slot = EIK_SLOT_PEXPRB43_1; T.info_idx = 0;
-      st = engine_call(grid, sm, SA, T, Wk);
-      if (st != EIK_OK) break;
-      double4 *W0 = A.W[0], *W1 = A.W[1];
-      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
+      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                     [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
+    } else if (key == EIK_PEXPRB43 * 4 + 1) {
+      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
       grid.sync();
-      st = phase_dev(grid, sm, S, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
-                     Wk.part);
-      if (st != EIK_OK) break;
-      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W1[i]; });  // U3
+      st = phase_dev(grid, sm, A.S1, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
+                     A.Wk.part);
+      if (st == EIK_OK) {
+        pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[1][i]; });  // U3
+        grid.sync();
+        st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                       [&](int64_t i, double4 d3) {
+                         const double4 a = d2[i];
+                         va[i] = dt * ((16.0 * a) - (2.0 * d3));
+                         vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
+                       },
+                       A.Wk.part);
+      }
+    } else if (key == EIK_EXPRB53 * 4 + 1) {
+      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
       grid.sync();
-      st = phase_dev(grid, sm, S, Ub, A.fn,
-                     [&](int64_t i, double4 d3) {
-                       const double4 a = d2[i];
-                       va[i] = dt * ((16.0 * a) - (2.0 * d3));
-                       vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
-                     },
-                     Wk.part);
-      if (st != EIK_OK) break;
-      T = base_task(A);
-      T.p = 4; T.v[3] = va; T.v[4] = vb; T.ns = 1; T.rho[0] = 1.0; T.W[0] = A.W[2];
-      T.slot = EIK_SLOT_PEXPRB43_2; T.info_idx = 1;
-      st = engine_call(grid, sm, SA, T, Wk);
-      fin = A.W[2];
-      base = Ub;  // u_{n+1} = U3 + W2
-      break;
-    }
-    case EIK_EXPRB53: {
-      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
-      T.W[0] = A.W[0]; T.W[1] = A.W[1];
-      T.slot = EIK_SLOT_EXPRB53_1; T.info_idx = 0;
-      st = engine_call(grid, sm, SA, T, Wk);
-      if (st != EIK_OK) break;
-      double4 *W0 = A.W[0], *W1 = A.W[1], *W2 = A.W[2], *W3 = A.W[3];
-      pointwise(S.N, [&](int64_t i) { Ub[i] = u[i] + W0[i]; });
-      grid.sync();
-      st = phase_dev(grid, sm, S, Ub, A.fn,
-                     [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, Wk.part);
-      if (st != EIK_OK) break;
-      T = base_task(A);
-      T.p = 3; T.v[3] = va; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
-      T.W[0] = W2; T.W[1] = W3;
-      T.slot = EIK_SLOT_EXPRB53_2; T.info_idx = 1;
-      st = engine_call(grid, sm, SA, T, Wk);
-      if (st != EIK_OK) break;
+      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                     [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, A.Wk.part);
+    } else if (key == EIK_EXPRB53 * 4 + 2) {
       const double c1 = 27.0 / 25.0, c2 = 729.0 / 125.0, q3 = A.c09cube;
-      pointwise(S.N, [&](int64_t i) {
-        const double4 ph = make_double4(W2[i].x / 0.125, W2[i].y / 0.125,
-                                        W2[i].z / 0.125, W2[i].w / 0.125);
-        const double4 pn = make_double4(W3[i].x / q3, W3[i].y / q3, W3[i].z / q3,
-                                        W3[i].w / q3);
-        Ub[i] = ((u[i] + W1[i]) + c1 * ph) + c2 * pn;
+      pointwise(A.S1.N, [&](int64_t i) {
+        const double4 w2 = W[2][i], w3 = W[3][i];
+        const double4 ph = make_double4(w2.x / 0.125, w2.y / 0.125, w2.z / 0.125, w2.w / 0.125);
+        const double4 pn = make_double4(w3.x / q3, w3.y / q3, w3.z / q3, w3.w / q3);
+        Ub[i] = ((u[i] + W[1][i]) + c1 * ph) + c2 * pn;
       });
       grid.sync();
       const double e1 = 250.0 / 81.0, e2 = 500.0 / 27.0;
-      st = phase_dev(grid, sm, S, Ub, A.fn,
+      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
                      [&](int64_t i, double4 d3) {
                        const double4 a = d2[i];
                        va[i] = dt * ((18.0 * a) - (e1 * d3));
                        vb[i] = dt * ((-60.0 * a) + (e2 * d3));
                      },
-                     Wk.part);
-      if (st != EIK_OK) break;
-      T = base_task(A);
-      T.p = 4; T.v[1] = A.v1; T.v[3] = va; T.v[4] = vb; T.ns = 1; T.rho[0] = 1.0;
-      T.W[0] = A.W[4];
-      T.slot = EIK_SLOT_EXPRB53_3; T.info_idx = 2;
-      st = engine_call(grid, sm, SA, T, Wk);
-      fin = A.W[4];
-      break;
+                     A.Wk.part);
     }
-    default:
-      st = EIK_EINVAL;
+    pc.mark(PC_DEV);
+    if (st != EIK_OK) break;
+    switch (key) {
+      case EIK_RB_EULER * 4:
+        T.p = 1; T.v[1] = A.v1; T.W[0] = W[0]; T.slot = EIK_SLOT_RBE;
+        fin = W[0];
+        break;
+      case EIK_EPI3 * 4:
+        T.p = 2; T.v[1] = A.v1; T.v[2] = va; T.W[0] = W[0]; T.slot = EIK_SLOT_EPI3;
+        fin = W[0];
+        break;
+      case EIK_EXPRB42 * 4:
+        T.p = 1; T.v[1] = A.v1; T.rho[0] = 0.75; T.W[0] = W[0]; T.slot = EIK_SLOT_EXPRB42_1;
+        break;
+      case EIK_EXPRB42 * 4 + 1:
+        T.p = 3; T.v[1] = A.v1; T.v[3] = va; T.W[0] = W[1]; T.slot = EIK_SLOT_EXPRB42_2;
+        fin = W[1];
+        break;
+      case EIK_PEXPRB43 * 4:
+        T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 1.0;
+        T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_PEXPRB43_1;
+        break;
+      case EIK_PEXPRB43 * 4 + 1:
+        T.p = 4; T.v[3] = va; T.v[4] = vb; T.W[0] = W[2]; T.slot = EIK_SLOT_PEXPRB43_2;
+        fin = W[2];
+        base = Ub;  // u_{n+1} = U3 + W2
+        break;
+      case EIK_EXPRB53 * 4:
+        T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+        T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_EXPRB53_1;
+        break;
+      case EIK_EXPRB53 * 4 + 1:
+        T.p = 3; T.v[3] = va; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+        T.W[0] = W[2]; T.W[1] = W[3]; T.slot = EIK_SLOT_EXPRB53_2;
+        break;
+      case EIK_EXPRB53 * 4 + 2:
+        T.p = 4; T.v[1] = A.v1; T.v[3] = va; T.v[4] = vb; T.W[0] = W[4];
+        T.slot = EIK_SLOT_EXPRB53_3;
+        fin = W[4];
+        break;
+      default:
+        st = EIK_EINVAL;
+    }
+    if (st != EIK_OK) break;
+    st = engine_call(grid, sm, A.SD, T, A.Wk, nA);
+    pc.skip();
   }
   if (st == EIK_OK) {
     double4* uu = A.u;
     double4* up = A.uprev;
-    pointwise(S.N, [&](int64_t i) {
+    pointwise(A.S1.N, [&](int64_t i) {
       const double4 old = uu[i];
       const double4 nb = base[i] + fin[i];
       up[i] = old;
@@ -361,24 +361,20 @@ __global__ void __launch_bounds__(TPB, 1) k_swe_step(SweArgs A) {
 }
 
 // ------------------------------------------------------- API-level kernels
-__global__ void __launch_bounds__(TPB, 1) k_swe_rhs(SweArgs A) {
+__global__ void __launch_bounds__(TPB, MINB) k_swe_rhs(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  SweOp S = A.S;
-  S.lin = A.x;
-  int st = phase_rhs(grid, sm, S, A.x, A.out, nullptr, 0.0, false, A.Wk.part);
+  int st = phase_rhs(grid, sm, A.S1, A.x, A.out, nullptr, 0.0, false, A.Wk.part);
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB, 1) k_swe_jv(SweArgs A) {
+__global__ void __launch_bounds__(TPB, MINB) k_swe_jv(SweArgs A) {
   // A.x = linearisation state, A.va = direction, A.out = J v
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  SweOp S = A.S;
-  S.lin = A.x;
-  S.scale = 1.0;
+  const SweOp& S = A.S1;
   int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
   int64_t lo, hi;
   brange(S.N, lo, hi);
@@ -388,31 +384,49 @@ __global__ void __launch_bounds__(TPB, 1) k_swe_jv(SweArgs A) {
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB, 1) k_swe_nnz(SweArgs A) {
+__global__ void __launch_bounds__(TPB, MINB) k_swe_nnz(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  SweOp S = A.S;
-  S.lin = A.x;
-  int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
-  const double c = phase_count_nnz(grid, sm, S, A.Wk.part, A.dbg);
+  int st = phase_rhs(grid, sm, A.S1, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  const double c = phase_count_nnz(grid, sm, A.S1, A.Wk.part, A.dbg);
   if (blockIdx.x == 0 && threadIdx.x == 0) *A.nnz_out = c;
   set_status(A.status, st);
 }
 
-__global__ void __launch_bounds__(TPB, 1) k_swe_phipm(SweArgs A) {
+__global__ void __launch_bounds__(TPB, MINB) k_swe_phipm(SweArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  SweOp S = A.S;
-  S.lin = A.x;
-  int st = phase_rhs(grid, sm, S, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  int st = phase_rhs(grid, sm, A.S1, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
   if (st != EIK_OK) { set_status(A.status, st); return; }
-  EngineWork Wk = A.Wk;
-  Wk.nnz = (int64_t)phase_count_nnz(grid, sm, S, Wk.part);
-  S.scale = A.dt;
-  st = engine_call(grid, sm, S, A.task, Wk);
+  const int64_t nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);
+  st = engine_call(grid, sm, A.SD, A.task, A.Wk, nA);
   set_status(A.status, st);
+}
+
+
+// Krylov-loop microbenchmark: `reps` IOM2 sweeps of dimension A.scheme on the
+// direction A.va at the linearisation state A.x (no controller, no expm).
+__global__ void __launch_bounds__(TPB, MINB) k_swe_kbench(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const SweOp& S = A.SD;
+  phase_rhs(grid, sm, A.S1, A.x, A.fn, nullptr, 0.0, true, A.Wk.part);
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  int64_t mv = 0;
+  for (int r = 0; r < (int)A.tol; ++r) {
+    double q[1] = {0.0};
+    for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) q[0] += dot4(A.va[i], A.va[i]);
+    grid_reduce<1>(grid, sm, q, A.Wk.part);
+    if (S.tiled_ok) {
+      KrylovState ks = krylov_tiled(grid, sm, S, A.Wk, A.va, sqrt(q[0]), A.scheme, mv);
+      if (blockIdx.x == 0 && threadIdx.x == 0) *A.nnz_out = (double)ks.keep;
+    }
+  }
+  set_status(A.status, EIK_OK);
 }
 
 struct CsrArgs {
@@ -422,11 +436,11 @@ struct CsrArgs {
   int* status;
 };
 
-__global__ void __launch_bounds__(TPB, 1) k_csr_phipm(CsrArgs A) {
+__global__ void __launch_bounds__(TPB, MINB) k_csr_phipm(CsrArgs A) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
-  const int st = engine_call(grid, sm, A.C, A.task, A.Wk);
+  const int st = engine_call(grid, sm, A.C, A.task, A.Wk, A.Wk.nnz);
   if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = st;
 }
 
@@ -505,6 +519,7 @@ struct EngineHost {
       CK(cudaFuncSetAttribute(kernels[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)std::max<size_t>(smem, 1)));
     G = coop_grid(kernels, nk, dev, NU, smem);
+    wk.dsm_bytes = (int64_t)smem;
     if (G_override > 0) {
       if (G_override > G)
         return fail(EIK_ECUDA, "cooperative grid does not fit the device");
@@ -649,10 +664,14 @@ struct EikSwe {
   float last_ms = 0.0f;
   double* pinned = nullptr;  // pinned staging for host copies (4N doubles)
 
-  SweArgs args() {
+  SweArgs args(double4* lin = nullptr, double dt = 1.0) {
     SweArgs A;
     memset(&A, 0, sizeof(A));
-    A.S = S;
+    A.S1 = S;
+    A.S1.lin = lin ? lin : u;
+    A.S1.scale = 1.0;
+    A.SD = A.S1;
+    A.SD.scale = dt;
     A.Wk = eng.wk;
     A.u = u;
     A.uprev = uprev;
@@ -710,7 +729,7 @@ struct EikCsr {
 
 static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_rhs,
                                     (const void*)k_swe_jv, (const void*)k_swe_nnz,
-                                    (const void*)k_swe_phipm};
+                                    (const void*)k_swe_phipm, (const void*)k_swe_kbench};
 static const void* kCsrKernels[] = {(const void*)k_csr_phipm};
 
 extern "C" {
@@ -782,16 +801,60 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
         else if (Df.data[k] != 0.0) dfx[i] += 1;
       }
   }
+  // ---- compact (off-diagonal) stencil for the tiled Krylov pass, valid when
+  // G, V, L rows sum to zero and D's diagonal is + the off-diagonal sum
+  int KC = 1;
+  std::vector<int32_t> offn((size_t)KMAX * N);
+  std::vector<int32_t> offc(N);
+  bool tiled_ok = true;
+  for (int64_t i = 0; i < N; ++i) {
+    int q = 0;
+    for (int s2 = 0; s2 < cnt[i]; ++s2)
+      if (cols[i][s2] != i) offn[(size_t)q++ * N + i] = cols[i][s2];
+    offc[i] = q;
+    KC = std::max(KC, q);
+    for (int o = 0; o < NOPS && tiled_ok; ++o) {
+      double off = 0.0, mag = 0.0, dg = 0.0;
+      for (int s2 = 0; s2 < cnt[i]; ++s2) {
+        const double v = coef[((size_t)s2 * NOPS + o) * N + i];
+        if (cols[i][s2] == i) dg = v;
+        else { off += v; mag += std::fabs(v); }
+      }
+      const double want = (o >= OP_DX && o <= OP_DZ) ? off : -off;
+      if (std::fabs(dg - want) > 1e-10 * mag + 1e-300) tiled_ok = false;
+    }
+  }
+  if (KC > KCMAX) tiled_ok = false;
+  KC = std::min(KC, KCMAX);
+  for (int64_t i = 0; i < N; ++i)
+    for (int q = offc[i]; q < KMAX; ++q) offn[(size_t)q * N + i] = (int32_t)i;
+  std::vector<double> coefc((size_t)KCMAX * 9 * N, 0.0);
+  std::vector<double> Lc((size_t)N * 8, 0.0);
+  // compact op order: Vx Vy Vz Gx Gy Gz Dx Dy Dz
+  const int corder[9] = {OP_VX, OP_VY, OP_VZ, OP_GX, OP_GY, OP_GZ, OP_DX, OP_DY, OP_DZ};
+  for (int64_t i = 0; i < N; ++i) {
+    int q = 0;
+    for (int s2 = 0; s2 < cnt[i] && q < KC; ++s2) {
+      if (cols[i][s2] == i) continue;
+      for (int k = 0; k < 9; ++k)
+        coefc[((size_t)q * 9 + k) * N + i] = coef[((size_t)s2 * NOPS + corder[k]) * N + i];
+      Lc[(size_t)i * 8 + q] = coef[((size_t)s2 * NOPS + OP_L) * N + i];
+      ++q;
+    }
+  }
+
   // ---- tiles along the Hilbert order, one CTA per SM, each tile <= TPB own
   // cells plus its 2-ring halo (local indices into shared memory)
   int nsm = 0;
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
     return fail(EIK_ECUDA, "no CUDA device");
-  const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (N + TPB - 1) / TPB));
-  const int64_t per = (N + (int64_t)Gt * TPB - 1) / ((int64_t)Gt * TPB);
+  const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * MINB, (N + TILE - 1) / TILE));
+  const int64_t per = (N + (int64_t)Gt * TILE - 1) / ((int64_t)Gt * TILE);
   const int NT = (int)(Gt * per);
-  const int64_t tsz = (N + NT - 1) / NT;
+  int64_t tsz = (N + NT - 1) / NT;
+  if (tsz & 1) ++tsz;  // even tiles keep the TMA runs 16-byte aligned
+  const int tma_ok = (EIK_TMA && tiled_ok && (N % 2 == 0)) ? 1 : 0;
   std::vector<int32_t> t_cell0(NT), t_nT(NT), t_nE1(NT), t_nE2(NT), t_e2off(NT), t_e1off(NT);
   std::vector<int32_t> e2map;
   std::vector<int16_t> lnbr;
@@ -824,7 +887,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
       for (int c2 = 0; c2 < nE1; ++c2) {
         const int32_t gi = list[c2];
         for (int q = 0; q < 8; ++q) {
-          const int32_t j = q < K ? nbr[(size_t)q * N + gi] : gi;
+          const int32_t j = q < KMAX ? offn[(size_t)q * N + gi] : gi;
           lnbr.push_back((int16_t)loc[j]);
         }
       }
@@ -833,16 +896,12 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
       e2max = std::max(e2max, nE2);
     }
   }
-  std::vector<double> Lc((size_t)N * 8, 0.0);
-  for (int64_t i = 0; i < N; ++i)
-    for (int q = 0; q < K; ++q) Lc[(size_t)i * 8 + q] = coef[((size_t)q * NOPS + OP_L) * N + i];
-
   EikSwe* c = new EikSwe();
   c->N = N;
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
   eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
-                             kSweKernels, 5, tile_smem_bytes(e1max, e2max), Gt);
+                             kSweKernels, 6, tile_smem_bytes(e1max, e2max, tma_ok), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
   int *d_nbr, *d_dfx, *d_cnt;
@@ -882,6 +941,9 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&d_e2map, e2map.size()));
   CKC(B.get(&d_lnbr, lnbr.size()));
   CKC(B.get(&d_Lc, Lc.size()));
+  double* d_coefc;
+  CKC(B.get(&d_coefc, coefc.size()));
+  CKC(cudaMemcpy(d_coefc, coefc.data(), coefc.size() * 8, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_tc0, t_cell0.data(), NT * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_tnT, t_nT.data(), NT * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_tnE1, t_nE1.data(), NT * 4, cudaMemcpyHostToDevice));
@@ -942,6 +1004,15 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.e2map = d_e2map;
   S.lnbr = d_lnbr;
   S.Lc = d_Lc;
+  S.coefc = d_coefc;
+  S.KC = KC;
+  S.tiled_ok = tiled_ok ? 1 : 0;
+  S.tma = tma_ok;
+  S.prof = nullptr;
+  if (EIK_PROF) {
+    unsigned long long* pr;
+    if (B.get(&pr, 4) == cudaSuccess) S.prof = pr;
+  }
   S.e1max = e1max;
   S.e2max = e2max;
   *out = c;
@@ -992,7 +1063,7 @@ eik_status eik_swe_rhs(EikSwe* c, const double* u, double* out) {
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
   if (s != EIK_OK) return s;
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->x);
   if ((s = c->launch((const void*)k_swe_rhs, A)) != EIK_OK) return s;
   if ((s = c->status()) != EIK_OK) return s;
   return c->d2h_cells(c->out, out);
@@ -1004,7 +1075,7 @@ eik_status eik_swe_jv(EikSwe* c, const double* u, const double* v, double* out) 
   eik_status s = c->h2d_cells(u, c->x);
   if (s == EIK_OK) s = c->h2d_cells(v, c->va);
   if (s != EIK_OK) return s;
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->x);
   if ((s = c->launch((const void*)k_swe_jv, A)) != EIK_OK) return s;
   if ((s = c->status()) != EIK_OK) return s;
   return c->d2h_cells(c->out, out);
@@ -1016,7 +1087,7 @@ eik_status eik_swe_jac_nnz_rows(EikSwe* c, const double* u, int64_t* nnz,
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
   if (s != EIK_OK) return s;
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->x);
   A.dbg = per_cell ? c->soa : nullptr;
   if ((s = c->launch((const void*)k_swe_nnz, A)) != EIK_OK) return s;
   if ((s = c->status()) != EIK_OK) return s;
@@ -1032,7 +1103,7 @@ eik_status eik_swe_jac_nnz(EikSwe* c, const double* u, int64_t* nnz) {
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
   if (s != EIK_OK) return s;
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->x);
   if ((s = c->launch((const void*)k_swe_nnz, A)) != EIK_OK) return s;
   if ((s = c->status()) != EIK_OK) return s;
   double v = 0.0;
@@ -1054,7 +1125,7 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
   for (int l = 0; l <= task->p; ++l)
     if (task->v && task->v[l] && (s = c->h2d_cells(task->v[l], E.vin[l])) != EIK_OK) return s;
   if (trace && trace_cap > 0 && (s = E.ensure_trace(trace_cap)) != EIK_OK) return s;
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->x, dt);
   A.dt = dt;
   A.task = E.make_task(task);
   A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
@@ -1069,7 +1140,7 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
 }
 
 static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol) {
-  SweArgs A = c->args();
+  SweArgs A = c->args(c->u, dt);
   A.dt = dt;
   A.tol = tol;
   A.scheme = scheme;
@@ -1176,6 +1247,65 @@ eik_status eik_swe_reset_seeds(EikSwe* c) {
   return c->eng.reset_seeds();
 }
 
+
+eik_status eik_swe_krylov_bench(EikSwe* c, const double* u, const double* v, double dt,
+                                int32_t m, int32_t reps, double* out) {
+  if (!c || !u || !v || !out || m < 1 || reps < 1) return fail(EIK_EINVAL, "invalid arguments");
+  if (m > c->eng.m_alloc) return fail(EIK_EINVAL, "m exceeds the basis allocation");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = c->h2d_cells(u, c->x);
+  if (s == EIK_OK) s = c->h2d_cells(v, c->va);
+  if (s != EIK_OK) return s;
+  SweArgs A = c->args(c->x, dt);
+  A.dt = dt;
+  A.scheme = m;
+  A.tol = 1.0;  // warm-up launch: one sweep
+  if ((s = c->launch((const void*)k_swe_kbench, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  A.tol = (double)reps;
+  CK(cudaEventRecord(c->ev0, c->eng.st));
+  if ((s = c->launch((const void*)k_swe_kbench, A)) != EIK_OK) return s;
+  CK(cudaEventRecord(c->ev1, c->eng.st));
+  if ((s = c->status()) != EIK_OK) return s;
+  float ms = 0.0f;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  double keep = 0.0;
+  CK(cudaMemcpy(&keep, c->eng.nnz_d, sizeof(double), cudaMemcpyDeviceToHost));
+  out[0] = ms;
+  out[1] = keep;
+  return EIK_OK;
+}
+
+eik_status eik_swe_info(const EikSwe* c, int64_t* out) {
+  if (!c || !out) return fail(EIK_EINVAL, "invalid arguments");
+  out[0] = c->eng.G;
+  out[1] = TPB;
+  out[2] = c->S.ntiles;
+  out[3] = c->S.e1max;
+  out[4] = c->S.e2max;
+  out[5] = c->S.K;
+  out[6] = c->S.KC;
+  out[7] = c->S.tiled_ok;
+  out[8] = (int64_t)c->eng.smem;
+  if (c->S.prof) {
+    unsigned long long pv[4];
+    cudaMemcpy(pv, c->S.prof, sizeof(pv), cudaMemcpyDeviceToHost);
+    for (int k = 0; k < 4; ++k) out[9 + k] = (int64_t)pv[k];
+  }
+  return EIK_OK;
+}
+
+int eik_prof_read(double* out, int reset) {
+  unsigned long long v[PC_N];
+  if (cudaMemcpyFromSymbol(v, g_prof, sizeof(v)) != cudaSuccess) return EIK_ECUDA;
+  for (int k = 0; k < PC_N; ++k) out[k] = (double)v[k];
+  if (reset) {
+    memset(v, 0, sizeof(v));
+    if (cudaMemcpyToSymbol(g_prof, v, sizeof(v)) != cudaSuccess) return EIK_ECUDA;
+  }
+  return EIK_PROF ? EIK_OK : EIK_EINVAL;
+}
+
 int64_t eik_swe_launches(const EikSwe* c) { return c ? c->eng.launches : 0; }
 double eik_swe_last_kernel_ms(const EikSwe* c) { return c ? (double)c->last_ms : 0.0; }
 int64_t eik_swe_krylov_iters(const EikSwe* c) {
@@ -1197,7 +1327,7 @@ eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max
   EikCsr* c = new EikCsr();
   const int64_t NU = (n + 3) / 4;
   eik_status s = c->eng.init(device, NU, n, std::min<int64_t>(std::max(m_max, 1), n),
-                             kCsrKernels, 1);
+                             kCsrKernels, 1, kDenseSmemBytes);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   int *rp, *ci;
   double* val;

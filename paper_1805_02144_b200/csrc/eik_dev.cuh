@@ -25,19 +25,48 @@ namespace cg = cooperative_groups;
 
 namespace eik {
 
-constexpr int TPB = 512;        // one CTA of 16 warps per SM (<=128 regs)
+#ifndef EIK_TPB
+#define EIK_TPB 256
+#endif
+#ifndef EIK_MINB
+#define EIK_MINB 2
+#endif
+constexpr int TPB = EIK_TPB;    // threads per CTA
+constexpr int MINB = EIK_MINB;  // co-resident CTAs per SM (register budget)
 constexpr int NWARP = TPB / 32;
 constexpr int NPART = 8;   // doubles per CTA partial record
 constexpr int MAXV = 8;    // v_0..v_7
 constexpr int MAXNS = 8;   // output points
 constexpr int MAXDIM = kDenseCap;
 constexpr int KMAX = 8;    // stencil slots per cell (self + up to 7)
+constexpr int KCMAX = 6;   // off-diagonal slots of the compact stencil (hexagons)
 constexpr int NOPS = 10;
 // Gram-identity norm of the orthogonalised vector is used while it keeps
 // h^2 > kGramSafe ||z||^2 (relative error of h below ~1e-14); else an
 // explicit orthogonalisation pass recomputes it.
 constexpr double kGramSafe = 1e-2;   // Gx Gy Gz Dx Dy Dz Vx Vy Vz L
 enum { OP_GX = 0, OP_GY, OP_GZ, OP_DX, OP_DY, OP_DZ, OP_VX, OP_VY, OP_VZ, OP_L };
+
+// ------------------------------------------------------------ profiling
+// EIK_PROF builds: CTA 0 / thread 0 accumulates clock64() deltas per phase
+// category (read back with eik_prof_read); zero cost otherwise.
+enum { PC_RHS = 0, PC_NNZ, PC_WREC, PC_KRYLOV, PC_DENSE, PC_CAND, PC_DEV, PC_MISC, PC_N = 16 };
+__device__ unsigned long long g_prof[PC_N];
+struct ProfClock {
+#if EIK_PROF && defined(__CUDA_ARCH__)
+  long long t;
+  __device__ ProfClock() : t(clock64()) {}
+  __device__ void mark(int k) {
+    const long long n = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_prof[k] += (unsigned long long)(n - t);
+    t = n;
+  }
+  __device__ void skip() { t = clock64(); }
+#else
+  __device__ void mark(int) {}
+  __device__ void skip() {}
+#endif
+};
 
 // ------------------------------------------------------------ double4 math
 __device__ __forceinline__ double4 d4(double a) { return make_double4(a, a, a, a); }
@@ -73,7 +102,9 @@ struct Smem {
   double tot[NPART];
   double phi[MAXDIM + 4];
   int ival[4];
-  int par;  // partial-buffer parity (double buffering, see grid_reduce)
+  int par;      // partial-buffer parity (double buffering, see grid_reduce)
+  int bar_init; // tile mbarrier initialised
+  int tphase;   // tile mbarrier phase
 };
 
 __device__ __forceinline__ void brange(int64_t NU, int64_t& lo, int64_t& hi) {
@@ -182,8 +213,13 @@ struct SweOp {
   const int* t_e2off;    // offset into e2map
   const int* t_e1off;    // offset into lnbr (rows)
   const int* e2map;      // local -> global cell id, order [own, H1, H2]
-  const short* lnbr;     // [rows][8] local neighbour slots of E1 cells
-  const double* Lc;      // [N][8] Laplacian row in slot order (cell-major)
+  const short* lnbr;     // [rows][8] local off-diagonal neighbours of E1 cells
+  const double* coefc;   // [KC][9][N] off-diagonal G, D, V (compact stencil)
+  const double* Lc;      // [N][8] off-diagonal Laplacian row (cell-major)
+  int KC;                // off-diagonal slots
+  int tiled_ok;          // compact stencil valid for this operator set
+  int tma;               // stage own-cell coefficients with TMA bulk copies
+  unsigned long long* prof;  // EIK_PROF builds: per-step cycle counters
   int e1max, e2max;
 
   static constexpr bool kTiled = true;
@@ -300,27 +336,137 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
 
 
 // ------------------------------------------------------------ tiled pass
+// The tiled Krylov pass works on the compact ("difference form") stencil:
+// for operators whose diagonal is minus (G, V, L) or plus (D) the sum of
+// the row's off-diagonal entries -- true for the sphere grid and for the
+// reference's planar operators -- only the off-diagonal slots are stored and
+//   (G e)_i = sum_j G_ij (e_j - e_i),  (D f)_i = sum_j D_ij (f_j + f_i).
 // Dynamic shared memory of one CTA: the tile's vector on E2, its Laplacian
 // and the linearisation state on E1, the E2 local->global map.
+#ifndef EIK_TMA
+#define EIK_TMA 0
+#endif
+// threads per own cell in the J v step (2: each thread does half the slots)
+#ifndef EIK_TPC
+#define EIK_TPC (EIK_TMA == 2 ? 2 : 1)
+#endif
+constexpr int TPC = EIK_TPC;
+constexpr int TILE = TPB / TPC;  // max own cells per tile
+#ifndef EIK_PROF
+#define EIK_PROF 0
+#endif
+constexpr int NCOEF = KCMAX * 9;  // staged coefficient chunks (slot-major G/D/V)
+
+#ifndef EIK_SPLIT
+#define EIK_SPLIT 1
+#endif
+// A double4 array in shared memory.  With EIK_SPLIT the (x,y) and (z,w)
+// halves live in two double2 arrays: a warp's random 16-byte reads then
+// spread over all 8 bank groups instead of the 4 a 32-byte stride allows.
+struct SArr {
+  double2* p;
+  int n;
+};
+__device__ __forceinline__ double4 sld(const SArr& a, int l) {
+#if EIK_SPLIT
+  const double2 u = a.p[l], v = a.p[a.n + l];
+  return make_double4(u.x, u.y, v.x, v.y);
+#else
+  return reinterpret_cast<const double4*>(a.p)[l];
+#endif
+}
+__device__ __forceinline__ void sst(const SArr& a, int l, double4 v) {
+#if EIK_SPLIT
+  a.p[l] = make_double2(v.x, v.y);
+  a.p[a.n + l] = make_double2(v.z, v.w);
+#else
+  reinterpret_cast<double4*>(a.p)[l] = v;
+#endif
+}
+
 struct TileSmem {
-  double4* x;
-  double4* La;
-  double4* U;
+  unsigned long long* bar;  // [2] mbarriers: A = small own-cell blocks, B = coefficients
+  double* cb;               // [NCOEF][TILE] own-cell coefficients (TMA)
+  double4* neb;             // [TILE] own-cell (n, eta) (TMA)
+  double4* vmb;             // [TILE] own-cell v_{j-1} (TMA, EIK_TMA == 2)
+  short* rowb;              // [TILE][8] own-cell local neighbour rows (TMA == 2)
+  double* lcb;              // [TILE][8] own-cell Laplacian rows (TMA == 2)
+  SArr x;
+  SArr La;
+  SArr U;
   int* gid;
 };
 
+__host__ __device__ constexpr size_t tile_tma_bytes(int tma) {
+  return tma == 0 ? 0
+                  : (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
+                        (tma == 2 ? (size_t)TILE * (32 + 16 + 64) : 0);
+}
+
 __device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+  extern __shared__ __align__(128) unsigned char dsm[];
   TileSmem t;
-  t.x = reinterpret_cast<double4*>(dsm);
-  t.La = t.x + S.e2max;
-  t.U = t.La + S.e1max;
-  t.gid = reinterpret_cast<int*>(t.U + S.e1max);
+  t.bar = reinterpret_cast<unsigned long long*>(dsm);
+  unsigned char* p = dsm + 128;
+  t.cb = reinterpret_cast<double*>(p);
+  unsigned char* p2 = p + (size_t)NCOEF * TILE * 8;
+  t.neb = reinterpret_cast<double4*>(p2);
+  p2 += (size_t)TILE * 32;
+  t.vmb = reinterpret_cast<double4*>(p2);
+  p2 += (size_t)TILE * 32;
+  t.lcb = reinterpret_cast<double*>(p2);
+  p2 += (size_t)TILE * 64;
+  t.rowb = reinterpret_cast<short*>(p2);
+  p += tile_tma_bytes(S.tma);
+  double2* q = reinterpret_cast<double2*>(p);
+  t.x = SArr{q, S.e2max};
+  q += 2 * S.e2max;
+  t.La = SArr{q, S.e1max};
+  q += 2 * S.e1max;
+  t.U = SArr{q, S.e1max};
+  q += 2 * S.e1max;
+  t.gid = reinterpret_cast<int*>(q);
   return t;
 }
 
-__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
-  return (size_t)e2max * 32 + (size_t)e1max * 64 + (size_t)e2max * 4 + 16;
+__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max, int tma) {
+  return 128 + tile_tma_bytes(tma) + (size_t)e2max * 32 + (size_t)e1max * 64 +
+         (size_t)e2max * 4 + 16;
+}
+
+// ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t bytes,
+                                        unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 struct Row8 {
@@ -333,102 +479,266 @@ __device__ __forceinline__ Row8 load_row8(const short* p) {
   return r;
 }
 
-// J x for own cell `c` of the tile (x, La, U staged in smem)
-__device__ __forceinline__ double4 swe_jv_tile(const SweOp& S, const TileSmem& ts,
-                                               const Row8& row, int c, int64_t i) {
-  double zeta = 0.0, gx = 0.0, gy = 0.0, gz = 0.0, dv = 0.0;
-  double4 ll = d4(0.0);
+// compact coefficient order in coefc: [KCMAX][9][N], ops Vx Vy Vz Gx Gy Gz Dx Dy Dz.
+// Partial J x sums over slots [s0, s0+ns) for own cell `c` (x, La, U in smem).
+struct JvAcc {
+  double zeta, gx, gy, gz, dv, l0, l1, l2, l3;
+};
+
+template <int kSrc, int NS>
+__device__ __forceinline__ JvAcc swe_jv_part(const SweOp& S, const TileSmem& ts, const short* row,
+                                             const double* lc, int s0, int c, int64_t i,
+                                             double4 ai, double4 Ui, double4 lai) {
+  // kSrc: 0 = coefficients from global, 1 = from the TMA-staged smem block
+  const double ei = Ui.x * ai.x + Ui.y * ai.y + Ui.z * ai.z + S.g * ai.w;
+  const double fxi = Ui.w * ai.x + Ui.x * ai.w, fyi = Ui.w * ai.y + Ui.y * ai.w,
+               fzi = Ui.w * ai.z + Ui.z * ai.w;
+  JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t st = (int64_t)9 * S.N;
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s) {
-    if (s < S.K) {
-      const int l = row.s[s];
-      const double4 aj = ts.x[l];
-      const double4 U = ts.U[l];
-      const double4 la = ts.La[l];
-      const double* cp = S.coef + (int64_t)s * NOPS * S.N + i;
-      const double vx = __ldcs(cp + OP_VX * S.N), vy = __ldcs(cp + OP_VY * S.N),
-                   vz = __ldcs(cp + OP_VZ * S.N);
-      const double gcx = __ldcs(cp + OP_GX * S.N), gcy = __ldcs(cp + OP_GY * S.N),
-                   gcz = __ldcs(cp + OP_GZ * S.N);
-      const double dx = __ldcs(cp + OP_DX * S.N), dy = __ldcs(cp + OP_DY * S.N),
-                   dz = __ldcs(cp + OP_DZ * S.N);
-      const double l0 = __ldcs(cp + OP_L * S.N);
-      zeta += vx * aj.x + vy * aj.y + vz * aj.z;
-      const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
-      gx += gcx * e;
-      gy += gcy * e;
-      gz += gcz * e;
-      dv += dx * (U.w * aj.x + U.x * aj.w) + dy * (U.w * aj.y + U.y * aj.w) +
-            dz * (U.w * aj.z + U.z * aj.w);
-      ll.x += l0 * la.x;
-      ll.y += l0 * la.y;
-      ll.z += l0 * la.z;
-      ll.w += l0 * la.w;
+  for (int k = 0; k < NS; ++k) {
+    const int s = s0 + k;
+    const int l = row[s];
+    double vx, vy, vz, gcx, gcy, gcz, dx, dy, dz;
+    if constexpr (kSrc == 1) {
+      const double* cp = ts.cb + (s * 9) * TILE + c;
+      vx = cp[0]; vy = cp[TILE]; vz = cp[2 * TILE];
+      gcx = cp[3 * TILE]; gcy = cp[4 * TILE]; gcz = cp[5 * TILE];
+      dx = cp[6 * TILE]; dy = cp[7 * TILE]; dz = cp[8 * TILE];
+    } else {
+      const double* cp = S.coefc + i + s * st;
+      vx = __ldcs(cp); vy = __ldcs(cp + S.N); vz = __ldcs(cp + 2 * S.N);
+      gcx = __ldcs(cp + 3 * S.N); gcy = __ldcs(cp + 4 * S.N); gcz = __ldcs(cp + 5 * S.N);
+      dx = __ldcs(cp + 6 * S.N); dy = __ldcs(cp + 7 * S.N); dz = __ldcs(cp + 8 * S.N);
     }
+    const double l0 = lc[s];
+    const double4 aj = sld(ts.x, l);
+    const double4 U = sld(ts.U, l);
+    const double4 la = sld(ts.La, l);
+    a.zeta += vx * (aj.x - ai.x) + vy * (aj.y - ai.y) + vz * (aj.z - ai.z);
+    const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
+    a.gx += gcx * (e - ei);
+    a.gy += gcy * (e - ei);
+    a.gz += gcz * (e - ei);
+    a.dv += dx * ((U.w * aj.x + U.x * aj.w) + fxi) + dy * ((U.w * aj.y + U.y * aj.w) + fyi) +
+            dz * ((U.w * aj.z + U.z * aj.w) + fzi);
+    a.l0 += l0 * (la.x - lai.x);
+    a.l1 += l0 * (la.y - lai.y);
+    a.l2 += l0 * (la.z - lai.z);
+    a.l3 += l0 * (la.w - lai.w);
   }
-  const double4 ai = ts.x[c];
-  const double4 U = ts.U[c];
-  const double4 q = S.ne[i];
-  const double px = q.y * U.z - q.z * U.y;
-  const double py = q.z * U.x - q.x * U.z;
-  const double pz = q.x * U.y - q.y * U.x;
+  return a;
+}
+
+__device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a, double4 q,
+                                                 double4 ai, double4 Ui) {
+  const double px = q.y * Ui.z - q.z * Ui.y;
+  const double py = q.z * Ui.x - q.x * Ui.z;
+  const double pz = q.x * Ui.y - q.y * Ui.x;
   const double cx = q.y * ai.z - q.z * ai.y;
   const double cy = q.z * ai.x - q.x * ai.z;
   const double cz = q.x * ai.y - q.y * ai.x;
   double4 r;
-  r.x = -(px * zeta) - q.w * cx - gx - S.nu * ll.x;
-  r.y = -(py * zeta) - q.w * cy - gy - S.nu * ll.y;
-  r.z = -(pz * zeta) - q.w * cz - gz - S.nu * ll.z;
-  r.w = -dv - S.nu * ll.w;
+  r.x = -(px * a.zeta) - q.w * cx - a.gx - S.nu * a.l0;
+  r.y = -(py * a.zeta) - q.w * cy - a.gy - S.nu * a.l1;
+  r.z = -(pz * a.zeta) - q.w * cz - a.gz - S.nu * a.l2;
+  r.w = -a.dv - S.nu * a.l3;
   return r;
 }
 
-// One pass over every tile: x = form(g, own) on E2 -> smem, L x on E1,
-// z = scale * J x on the own cells -> epi(i, c, z, x_i).  A whole Krylov
-// iteration (orthogonalise + normalise v_j, L v_j, J v_j, projections) is
-// one such pass: one HBM sweep and one grid barrier per iteration.
-template <class Form, class Epi>
-__device__ void swe_tiled(const SweOp& S, const Form& form, const Epi& epi) {
+// How a tiled pass builds its input vector on the fly at every E2 cell:
+//   x = ((src - a1 * vm2) - a2 * vm1) / h     (vm2 / vm1 optional)
+// i.e. the MGS update and normalisation of krylov.py:91-104 fused into the
+// load; own cells also store x (the new basis vector) to `out`.
+struct Form {
+  const double4* src;
+  const double4* vm2;
+  const double4* vm1;
+  double a1, a2, h;
+  double4* out;
+  const double4* epi_vm1;  // own-cell vector handed to the epilogue (may be null)
+};
+
+__device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
+                                          double4 s2) {
+  double4 x = s0;
+  if (f.vm2) x = x - f.a1 * s1;
+  if (f.vm1) x = x - f.a2 * s2;
+  return div4(x, f.h);
+}
+
+// One pass over every tile: x on E2 -> smem, L x on E1, z = scale * J x on
+// the own cells -> epi(i, z, x_i).  A whole Krylov iteration (orthogonalise
+// + normalise v_j, L v_j, J v_j, projections) is one such pass: one HBM
+// sweep and one grid barrier per iteration.
+template <class Epi>
+__device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
   const TileSmem ts = tile_smem(S);
+  const int tma = S.tma;
+  if (tma && threadIdx.x == 0 && !sm.bar_init) {
+    mbar_init(ts.bar, 1);
+    mbar_init(ts.bar + 1, 1);
+    sm.bar_init = 1;
+  }
+  __syncthreads();
+  uint32_t ph = (uint32_t)sm.tphase;  // per-thread copy of the mbarrier phase
+#if EIK_PROF
+  long long pt0 = clock64(), pt1, pacc[4] = {0, 0, 0, 0};
+#endif
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+    if (nT == 0) continue;  // uniform over the CTA
     const int* map = S.e2map + __ldg(S.t_e2off + t);
     const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-    for (int c = threadIdx.x; c < nE2; c += TPB) {
-      const int g = __ldg(map + c);
-      ts.gid[c] = g;
-      ts.x[c] = form(g, c < nT);
-      if (c < nE1) ts.U[c] = S.lin[g];
+    if (tma && threadIdx.x < 32) {
+      // stage the tile's own-cell blocks (contiguous runs: own cells are a
+      // contiguous Hilbert range) in shared memory with bulk copies while the
+      // gathers of steps 1-2 are in flight.  A: small blocks, B: coefficients.
+      fence_proxy_async_shared();
+      const uint32_t run = (uint32_t)nT * 8;
+      const bool vmx = (tma == 2) && F.epi_vm1 != nullptr;
+      if (threadIdx.x == 0) {
+        if (tma == 2)
+          mbar_expect_tx(ts.bar, (uint32_t)nT * (32 + 16 + 64) + (vmx ? (uint32_t)nT * 32 : 0u));
+        mbar_expect_tx(ts.bar + 1, run * NCOEF + (tma == 1 ? (uint32_t)nT * 32 : 0u));
+      }
+      __syncwarp();
+      if (tma == 2 && threadIdx.x == 0) {
+        tma_g2s(ts.neb, S.ne + c0, (uint32_t)nT * 32, ts.bar);
+        tma_g2s(ts.rowb, rows, (uint32_t)nT * 16, ts.bar);
+        tma_g2s(ts.lcb, S.Lc + c0 * 8, (uint32_t)nT * 64, ts.bar);
+        if (vmx) tma_g2s(ts.vmb, F.epi_vm1 + c0, (uint32_t)nT * 32, ts.bar);
+      }
+      for (int q = threadIdx.x; q < NCOEF; q += 32)
+        tma_g2s(ts.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run, ts.bar + 1);
+      if (tma == 1 && threadIdx.x == 0) tma_g2s(ts.neb, S.ne + c0, (uint32_t)nT * 32, ts.bar + 1);
     }
+    // step 1: x on E2 (two cells per thread per round, all loads issued first)
+    for (int base = 0; base < nE2; base += 2 * TPB) {
+      const int ca = base + threadIdx.x, cb = ca + TPB;
+      const bool va = ca < nE2, vb = cb < nE2;
+      const int ga = va ? __ldg(map + ca) : 0;
+      const int gb = vb ? __ldg(map + cb) : 0;
+      double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
+              b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
+      if (va) {
+        a0 = F.src[ga];
+        if (F.vm2) a1 = F.vm2[ga];
+        if (F.vm1) a2 = F.vm1[ga];
+        if (ca < nE1) ua = S.lin[ga];
+      }
+      if (vb) {
+        b0 = F.src[gb];
+        if (F.vm2) b1 = F.vm2[gb];
+        if (F.vm1) b2 = F.vm1[gb];
+        if (cb < nE1) ub = S.lin[gb];
+      }
+      if (va) {
+        const double4 x = form_x(F, a0, a1, a2);
+        ts.gid[ca] = ga;
+        sst(ts.x, ca, x);
+        if (ca < nE1) sst(ts.U, ca, ua);
+        if (F.out && ca < nT) F.out[ga] = x;
+      }
+      if (vb) {
+        const double4 x = form_x(F, b0, b1, b2);
+        ts.gid[cb] = gb;
+        sst(ts.x, cb, x);
+        if (cb < nE1) sst(ts.U, cb, ub);
+        if (F.out && cb < nT) F.out[gb] = x;
+      }
+    }
+    if (tma == 2) mbar_wait(ts.bar, ph);
     __syncthreads();
+#if EIK_PROF
+    pt1 = clock64(); pacc[0] += pt1 - pt0; pt0 = pt1;
+#endif
+    // step 2: L x on E1 (difference form)
     for (int c = threadIdx.x; c < nE1; c += TPB) {
-      const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
+      const bool own2 = (tma == 2) && c < nT;
+      const Row8 row = own2 ? *reinterpret_cast<const Row8*>(ts.rowb + c * 8)
+                            : load_row8(rows + (int64_t)c * 8);
+      const double* lc = own2 ? ts.lcb + c * 8 : S.Lc + (int64_t)ts.gid[c] * 8;
+      const double4 xc = sld(ts.x, c);
       double4 acc = d4(0.0);
 #pragma unroll
-      for (int s = 0; s < KMAX; ++s) {
-        if (s < S.K) {
-          const double l = __ldg(lc + s);
-          const double4 xv = ts.x[row.s[s]];
-          acc.x += l * xv.x;
-          acc.y += l * xv.y;
-          acc.z += l * xv.z;
-          acc.w += l * xv.w;
-        }
+      for (int s = 0; s < KCMAX; ++s) {
+        const double l = own2 ? lc[s] : __ldg(lc + s);
+        const double4 xv = sld(ts.x, row.s[s]);
+        acc.x += l * (xv.x - xc.x);
+        acc.y += l * (xv.y - xc.y);
+        acc.z += l * (xv.z - xc.z);
+        acc.w += l * (xv.w - xc.w);
       }
-      ts.La[c] = acc;
+      sst(ts.La, c, acc);
     }
     __syncthreads();
-    if (threadIdx.x < nT) {
-      const int c = threadIdx.x;
-      const int64_t i = c0 + c;
-      const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const double4 z = S.scale * swe_jv_tile(S, ts, row, c, i);
-      epi(i, z, ts.x[c]);
+#if EIK_PROF
+    pt1 = clock64(); pacc[1] += pt1 - pt0; pt0 = pt1;
+#endif
+    // step 3: z = scale * J x on the own cells (TPC threads per cell)
+    if (tma) mbar_wait(ts.bar + 1, ph);
+    ph ^= 1u;
+    {
+      const int c = threadIdx.x / TPC;
+      const int part = threadIdx.x % TPC;
+      const bool live = c < nT;
+      const int cc = live ? c : 0;
+      const int64_t i = c0 + cc;
+      const double4 ai = sld(ts.x, cc);
+      const double4 Ui = sld(ts.U, cc);
+      const double4 lai = sld(ts.La, cc);
+      JvAcc a;
+      if (tma == 2) {
+        a = swe_jv_part<1, KCMAX / TPC>(S, ts, ts.rowb + cc * 8, ts.lcb + cc * 8,
+                                         part * (KCMAX / TPC), cc, i, ai, Ui, lai);
+      } else {
+        const Row8 row = load_row8(rows + (int64_t)cc * 8);
+        const double* lc = S.Lc + i * 8;
+        double lcr[8];
+#pragma unroll
+        for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
+        if (tma == 1)
+          a = swe_jv_part<1, KCMAX / TPC>(S, ts, row.s, lcr, part * (KCMAX / TPC), cc, i, ai,
+                                           Ui, lai);
+        else
+          a = swe_jv_part<0, KCMAX / TPC>(S, ts, row.s, lcr, part * (KCMAX / TPC), cc, i, ai,
+                                           Ui, lai);
+      }
+      if constexpr (TPC == 2) {
+        a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
+        a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
+        a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
+        a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
+        a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
+        a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
+        a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
+        a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
+        a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
+      }
+      if (live && part == 0) {
+        const double4 q = tma ? ts.neb[cc] : S.ne[i];
+        const double4 z = S.scale * swe_jv_finish(S, a, q, ai, Ui);
+        const double4 vm = F.epi_vm1 ? (tma == 2 ? ts.vmb[cc] : F.epi_vm1[i]) : d4(0.0);
+        epi(i, z, ai, vm);
+      }
     }
     __syncthreads();
+#if EIK_PROF
+    pt1 = clock64(); pacc[2] += pt1 - pt0; pt0 = pt1;
+#endif
   }
+  if (threadIdx.x == 0) sm.tphase = (int)ph;
+  __syncthreads();
+#if EIK_PROF
+  if (threadIdx.x == 0 && S.prof) {
+    atomicAdd(S.prof + 0, (unsigned long long)pacc[0]);
+    atomicAdd(S.prof + 1, (unsigned long long)pacc[1]);
+    atomicAdd(S.prof + 2, (unsigned long long)pacc[2]);
+    atomicAdd(S.prof + 3, 1ull);
+  }
+#endif
 }
 
 struct SrcPtr {
@@ -491,14 +801,77 @@ __device__ __forceinline__ double4 op_main(const CsrOp& C, const double4* x4,
 // run by one CTA on an L2-resident scratch; LU with partial pivoting
 // (LAPACK dgesv semantics: first max |pivot|, reciprocal scaling).
 
-__device__ void blk_matmul(const double* A, const double* B, double* C, int n) {
-  for (int idx = threadIdx.x; idx < n * n; idx += TPB) {
-    const int i = idx / n, j = idx - i * n;
-    const double* a = A + (int64_t)i * n;
-    double s = 0.0;
-    for (int k = 0; k < n; ++k) s += a[k] * B[(int64_t)k * n + j];
-    C[idx] = s;
+// Dense scratch in shared memory for the single-CTA dense phase: the tile
+// buffers of the Krylov pass are dead by then (beyond the 128-byte header
+// that may hold the tile mbarriers).
+struct DenseSmem {
+  double* p;
+  int n;  // doubles available
+};
+__device__ __forceinline__ DenseSmem dense_smem(int64_t bytes) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  DenseSmem d;
+  d.p = reinterpret_cast<double*>(dsm + 128);
+  d.n = bytes > 256 ? (int)((bytes - 128) / 8) : 0;
+  return d;
+}
+
+constexpr int MMT = 32;  // dense matmul tile
+// C = A B (n x n, row-major, global/L2 scratch).  32x32 output tiles staged
+// through shared memory; each output is summed over k in ascending order.
+__device__ void blk_matmul(const double* A, const double* B, double* C, int n,
+                           const DenseSmem& ds) {
+  if (ds.n < 2 * MMT * (MMT + 1)) {
+    for (int idx = threadIdx.x; idx < n * n; idx += TPB) {
+      const int i = idx / n, j = idx - i * n;
+      const double* a = A + (int64_t)i * n;
+      double s = 0.0;
+      for (int k = 0; k < n; ++k) s += a[k] * B[(int64_t)k * n + j];
+      C[idx] = s;
+    }
+    __syncthreads();
+    return;
   }
+  constexpr int EPT = (MMT * MMT + TPB - 1) / TPB;
+  double* As = ds.p;
+  double* Bs = ds.p + MMT * (MMT + 1);
+  const int nt = (n + MMT - 1) / MMT;
+  for (int ti = 0; ti < nt; ++ti)
+    for (int tj = 0; tj < nt; ++tj) {
+      double acc[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) acc[e] = 0.0;
+      for (int tk = 0; tk < nt; ++tk) {
+        for (int e = threadIdx.x; e < MMT * MMT; e += TPB) {
+          const int r = e / MMT, c = e % MMT;
+          const int ia = ti * MMT + r, ka = tk * MMT + c;
+          const int kb = tk * MMT + r, jb = tj * MMT + c;
+          As[r * (MMT + 1) + c] = (ia < n && ka < n) ? A[(int64_t)ia * n + ka] : 0.0;
+          Bs[r * (MMT + 1) + c] = (kb < n && jb < n) ? B[(int64_t)kb * n + jb] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const int idx = threadIdx.x + e * TPB;
+          if (idx < MMT * MMT) {
+            const int r = idx / MMT, c = idx % MMT;
+            double s = acc[e];
+            const int kmax = min(MMT, n - tk * MMT);
+            for (int k = 0; k < kmax; ++k) s += As[r * (MMT + 1) + k] * Bs[k * (MMT + 1) + c];
+            acc[e] = s;
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int idx = threadIdx.x + e * TPB;
+        if (idx < MMT * MMT) {
+          const int i = ti * MMT + idx / MMT, j = tj * MMT + idx % MMT;
+          if (i < n && j < n) C[(int64_t)i * n + j] = acc[e];
+        }
+      }
+    }
   __syncthreads();
 }
 
@@ -523,7 +896,25 @@ __device__ double blk_norm1(Smem& sm, const double* M, int n) {
 }
 
 // Solve P X = Q in place (Q <- X), P overwritten by its LU factors.
-__device__ void blk_solve(Smem& sm, double* P, double* Q, int n) {
+__device__ void blk_solve_at(Smem& sm, double* P, double* Q, int n);
+__device__ void blk_solve(Smem& sm, double* P, double* Q, int n, const DenseSmem& ds) {
+  const int nn = n * n;
+  if (ds.n >= 2 * nn) {
+    double* Ps = ds.p;
+    double* Qs = ds.p + nn;
+    for (int idx = threadIdx.x; idx < nn; idx += TPB) {
+      Ps[idx] = P[idx];
+      Qs[idx] = Q[idx];
+    }
+    __syncthreads();
+    blk_solve_at(sm, Ps, Qs, n);
+    for (int idx = threadIdx.x; idx < nn; idx += TPB) Q[idx] = Qs[idx];
+    __syncthreads();
+  } else {
+    blk_solve_at(sm, P, Q, n);
+  }
+}
+__device__ void blk_solve_at(Smem& sm, double* P, double* Q, int n) {
   for (int k = 0; k < n; ++k) {
     // pivot: first index of max |P[i][k]|, i >= k (warp 0)
     if (threadIdx.x < 32) {
@@ -589,10 +980,13 @@ __device__ void blk_solve(Smem& sm, double* P, double* Q, int n) {
 
 // E = expm(M0) for the n x n matrix in M0; returns the index of the scratch
 // matrix holding E.  scratch: 6 matrices of MAXDIM^2.
-__device__ int blk_expm(Smem& sm, double* scr, int n) {
-  const int64_t S2 = (int64_t)MAXDIM * MAXDIM;
+// The matrices live in shared memory when 6 n^2 doubles fit (the common
+// case: n = m + p + 1 <= 46 with the SWE kernels' 102 KB dynamic smem),
+// else in the L2-resident global scratch `scr` (stride MAXDIM^2).  M[0]
+// holds the input on entry; returns the matrix holding exp(M[0]).
+__device__ double* blk_expm(Smem& sm, double** Mq, int n, const DenseSmem& ds) {
   double* M[6];
-  for (int q = 0; q < 6; ++q) M[q] = scr + q * S2;
+  for (int q = 0; q < 6; ++q) M[q] = Mq[q];
   const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                         1187353796428800.0, 129060195264000.0, 10559470521600.0,
                         670442572800.0, 33522128640.0, 1323241920.0, 40840800.0,
@@ -610,15 +1004,15 @@ __device__ int blk_expm(Smem& sm, double* scr, int n) {
     __syncthreads();
   }
   double *X = M[0], *X2 = M[1], *X4 = M[2], *X6 = M[3];
-  blk_matmul(X, X, X2, n);
-  blk_matmul(X2, X2, X4, n);
-  blk_matmul(X2, X4, X6, n);
+  blk_matmul(X, X, X2, n, ds);
+  blk_matmul(X2, X2, X4, n, ds);
+  blk_matmul(X2, X4, X6, n, ds);
   double* T = M[4];
   for (int idx = threadIdx.x; idx < nn; idx += TPB)
     T[idx] = b[13] * X6[idx] + b[11] * X4[idx] + b[9] * X2[idx];
   __syncthreads();
   double* T2 = M[5];
-  blk_matmul(X6, T, T2, n);
+  blk_matmul(X6, T, T2, n, ds);
   for (int idx = threadIdx.x; idx < nn; idx += TPB) {
     const int i = idx / n, j = idx - i * n;
     T2[idx] = T2[idx] + b[7] * X6[idx] + b[5] * X4[idx] + b[3] * X2[idx] +
@@ -626,13 +1020,13 @@ __device__ int blk_expm(Smem& sm, double* scr, int n) {
   }
   __syncthreads();
   double* U = M[4];  // T is dead
-  blk_matmul(X, T2, U, n);
+  blk_matmul(X, T2, U, n, ds);
   double* T3 = M[5];  // T2 is dead
   for (int idx = threadIdx.x; idx < nn; idx += TPB)
     T3[idx] = b[12] * X6[idx] + b[10] * X4[idx] + b[8] * X2[idx];
   __syncthreads();
   double* V = M[0];  // X is dead
-  blk_matmul(X6, T3, V, n);
+  blk_matmul(X6, T3, V, n, ds);
   for (int idx = threadIdx.x; idx < nn; idx += TPB) {
     const int i = idx / n, j = idx - i * n;
     const double v = V[idx] + b[6] * X6[idx] + b[4] * X4[idx] + b[2] * X2[idx] +
@@ -642,13 +1036,13 @@ __device__ int blk_expm(Smem& sm, double* scr, int n) {
     M[2][idx] = v + u;  // Q (X4 likewise)
   }
   __syncthreads();
-  blk_solve(sm, M[1], M[2], n);
+  blk_solve(sm, M[1], M[2], n, ds);
   int cur = 2, oth = 3;
   for (int q = 0; q < s; ++q) {
-    blk_matmul(M[cur], M[cur], M[oth], n);
+    blk_matmul(M[cur], M[cur], M[oth], n, ds);
     const int t = cur; cur = oth; oth = t;
   }
-  return cur;
+  return M[cur];
 }
 
 // =================================================================== engine
@@ -683,13 +1077,132 @@ struct EngineWork {
   int64_t* trace_len;
   unsigned long long* kiters;
   int64_t NU, n, nnz, m_alloc;
+  int64_t dsm_bytes;        // dynamic shared memory per CTA (dense phase scratch)
 };
+
+
+// Result of an IOM2 sweep: kept dimension, breakdown flag, h_{m+1,m} and the
+// recipe for v_{m+1} = ((vz - h1 vm1) - h2 vv) / hnext (or vz / hnext).
+struct KrylovState {
+  int64_t keep;
+  bool broke;
+  double hnext;
+  const double4* vz;
+  const double4* vm1;
+  const double4* vv;
+  double h1, h2;
+  bool expl;
+};
+
+// IOM2 (krylov.py:53-112) with one tiled pass + one grid barrier per
+// iteration: v_j is formed on the fly from (z_{j-1}, v_{j-2}, v_{j-1}) with
+// the previous iteration's MGS coefficients; its norm comes from the Gram
+// identity (explicit orthogonalisation pass only when that would cancel).
+// H (row-major, leading dimension m_alloc) is written by CTA 0.
+__device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp& op,
+                                    const EngineWork& Wk, const double4* wp, double beta,
+                                    int64_t m_eff, int64_t& mv) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int64_t NU = Wk.NU, ld = Wk.m_alloc;
+  int64_t lo, hi;
+  brange(NU, lo, hi);
+  KrylovState out;
+  out.keep = m_eff;
+  out.broke = false;
+  out.hnext = 0.0;
+  out.vz = Wk.zbuf;
+  out.vm1 = nullptr;
+  out.vv = nullptr;
+  out.h1 = out.h2 = 0.0;
+  out.expl = true;
+  double hcur = beta;
+        double h1 = 0.0, h2 = 0.0, nm1 = 0.0;
+        bool expl = false;
+        for (int64_t j = 0; j < m_eff; ++j) {
+          double4* vj = Wk.basis + j * NU;
+          const double4* vm1 = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
+          const double4* vm2 = j > 1 ? Wk.basis + (j - 2) * NU : nullptr;
+          const double4* zin = (j & 1) ? Wk.zbuf : Wk.zbuf2;
+          double4* zout = (j & 1) ? Wk.zbuf2 : Wk.zbuf;
+          double d[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+          const double hc = hcur, a1 = h1, a2 = h2;
+          Form F;
+          F.src = j == 0 ? wp : zin;
+          F.vm2 = (j == 0 || expl) ? nullptr : vm2;
+          F.vm1 = (j == 0 || expl) ? nullptr : vm1;
+          F.a1 = a1;
+          F.a2 = a2;
+          F.h = hc;
+          F.out = vj;
+          F.epi_vm1 = vm1;
+          swe_tiled(
+              sm, op, F,
+              [&](int64_t i, double4 z, double4 x, double4 b) {
+                zout[i] = z;
+                d[1] += dot4(x, z);
+                d[3] += dot4(z, z);
+                d[4] += dot4(x, x);
+                if (vm1) {
+                  d[0] += dot4(b, z);
+                  d[2] += dot4(x, b);
+                }
+              });
+          ++mv;
+          if (lead) atomicAdd(Wk.kiters, 1ull);
+          grid_reduce<5>(grid, sm, d, Wk.part);
+          const double h1n = vm1 ? d[0] : 0.0;
+          const double h2n = vm1 ? d[1] - h1n * d[2] : d[1];
+          if (lead) {
+            if (vm1) Wk.H[(j - 1) * ld + j] = h1n;
+            Wk.H[j * ld + j] = h2n;
+          }
+          double hsq = d[3] - 2.0 * h2n * d[1] + h2n * h2n * d[4];
+          if (vm1) hsq += -2.0 * h1n * d[0] + h1n * h1n * nm1 + 2.0 * h1n * h2n * d[2];
+          expl = !(hsq > kGramSafe * d[3]);
+          if (expl) {
+            double r[1] = {0.0};
+            for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+              double4 z = zout[u];
+              if (vm1) z = z - h1n * vm1[u];
+              z = z - h2n * vj[u];
+              zout[u] = z;
+              r[0] += dot4(z, z);
+            }
+            grid_reduce<1>(grid, sm, r, Wk.part);
+            hsq = r[0];
+            if (lead) atomicAdd(Wk.kiters + 1, 1ull);
+          }
+          const double h = sqrt(hsq);
+          nm1 = d[4];
+          if (h < kBreakdownTol * beta) {
+            out.broke = true;
+            out.keep = j + 1;
+            out.hnext = 0.0;
+            break;
+          }
+          if (j + 1 < m_eff) {
+            if (lead) Wk.H[(j + 1) * ld + j] = h;
+            hcur = h;
+            h1 = h1n;
+            h2 = h2n;
+          } else {
+            out.hnext = h;
+            out.vz = zout;
+            out.h1 = h1n;
+            out.h2 = h2n;
+            out.vm1 = vm1;
+            out.vv = vj;
+            out.expl = expl;
+          }
+        }
+  return out;
+}
 
 // phipm_simul_iom2 (phipm.py:291-370); returns an eik_status, uniformly in
 // every CTA.
 template <class Op>
 __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
-                           const EngineTask& T, const EngineWork& Wk) {
+                           const EngineTask& T, const EngineWork& Wk, int64_t nnz) {
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   const int64_t NU = Wk.NU, n = Wk.n;
   const int p = T.p;
@@ -769,6 +1282,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
       const bool hits = eik_add(t, tau) >= t_out;
       if (hits) tau = eik_sub(t_out, t);
 
+      ProfClock pc;
       // ---- w recurrence (phipm.py:159-182)
       const double4* wprev = y;
       bool wprev_nz = y_nz;
@@ -779,12 +1293,14 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         const bool do_mv = !(T.zero_skip && !wprev_nz);
         double4* wj = Wk.w[j];
         double r[2] = {0.0, 0.0};
+        bool tiled_mv = false;
+        if constexpr (Op::kTiled) tiled_mv = op.tiled_ok && do_mv;
         if constexpr (Op::kTiled) {
-          if (do_mv) {
+          if (tiled_mv) {
             ++mv;
-            const double4* src = wprev;
-            swe_tiled(op, [&](int64_t g, bool) { return src[g]; },
-                      [&](int64_t i, double4 z, double4) {
+            Form F{wprev, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+            swe_tiled(sm, op, F,
+                      [&](int64_t i, double4 z, double4, double4) {
                         double4 a = z;
                         for (int ell = 0; ell <= p - j; ++ell)
                           if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][i];
@@ -793,14 +1309,15 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
                         r[1] += dot4(a, a);
                       });
           }
-        } else {
+        }
+        if (!tiled_mv) {
           if (do_mv) {
             op_pre(op, wprev, 1.0, lo, hi);
             grid.sync();
             ++mv;
           }
         }
-        if (!Op::kTiled || !do_mv) {
+        if (!tiled_mv) {
           for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
             double4 a = do_mv ? op_main(op, wprev, u) : d4(0.0);
             for (int ell = 0; ell <= p - j; ++ell)
@@ -828,6 +1345,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
       }
       const double4* wp = wprev;
       const bool wp_nz = wprev_nz;
+      pc.mark(PC_WREC);
 
       // ---- IOM2 Krylov decomposition (krylov.py:53-112)
       double beta = 0.0, hnext = 0.0, eps = 0.0, nh = 0.0, corner = 0.0;
@@ -852,93 +1370,22 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         keep = m_eff;
         bool tiled_done = false;
         if constexpr (Op::kTiled) {
-          if (iom == 2) {
+          if (iom == 2 && op.tiled_ok) {
             tiled_done = true;
             // one tiled pass + one grid barrier per iteration: v_j is formed
             // on the fly from (z_{j-1}, v_{j-2}, v_{j-1}) with the previous
             // iteration's MGS coefficients, its norm taken from the Gram
             // identity (explicit pass only when that would cancel)
-            double h1 = 0.0, h2 = 0.0, nm1 = 0.0;
-            bool expl = false;
-            for (int64_t j = 0; j < m_eff; ++j) {
-              double4* vj = Wk.basis + j * NU;
-              const double4* vm1 = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
-              const double4* vm2 = j > 1 ? Wk.basis + (j - 2) * NU : nullptr;
-              const double4* zin = (j & 1) ? Wk.zbuf : Wk.zbuf2;
-              double4* zout = (j & 1) ? Wk.zbuf2 : Wk.zbuf;
-              double d[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-              const double hc = hcur, a1 = h1, a2 = h2;
-              const int mode = j == 0 ? 0 : (expl ? 0 : (vm2 ? 2 : 1));
-              const double4* src = j == 0 ? wp : zin;
-              swe_tiled(
-                  op,
-                  [&](int64_t g, bool own) {
-                    double4 x = src[g];
-                    if (mode == 2) x = x - a1 * vm2[g];
-                    if (mode >= 1) x = x - a2 * vm1[g];
-                    x = div4(x, hc);
-                    if (own) vj[g] = x;
-                    return x;
-                  },
-                  [&](int64_t i, double4 z, double4 x) {
-                    zout[i] = z;
-                    d[1] += dot4(x, z);
-                    d[3] += dot4(z, z);
-                    d[4] += dot4(x, x);
-                    if (vm1) {
-                      const double4 b = vm1[i];
-                      d[0] += dot4(b, z);
-                      d[2] += dot4(x, b);
-                    }
-                  });
-              ++mv;
-              if (lead) atomicAdd(Wk.kiters, 1ull);
-              grid_reduce<5>(grid, sm, d, Wk.part);
-              const double h1n = vm1 ? d[0] : 0.0;
-              const double h2n = vm1 ? d[1] - h1n * d[2] : d[1];
-              if (lead) {
-                if (vm1) Wk.H[(j - 1) * ld + j] = h1n;
-                Wk.H[j * ld + j] = h2n;
-              }
-              double hsq = d[3] - 2.0 * h2n * d[1] + h2n * h2n * d[4];
-              if (vm1) hsq += -2.0 * h1n * d[0] + h1n * h1n * nm1 + 2.0 * h1n * h2n * d[2];
-              expl = !(hsq > kGramSafe * d[3]);
-              if (expl) {
-                double r[1] = {0.0};
-                for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-                  double4 z = zout[u];
-                  if (vm1) z = z - h1n * vm1[u];
-                  z = z - h2n * vj[u];
-                  zout[u] = z;
-                  r[0] += dot4(z, z);
-                }
-                grid_reduce<1>(grid, sm, r, Wk.part);
-                hsq = r[0];
-                if (lead) atomicAdd(Wk.kiters + 1, 1ull);
-              }
-              const double h = sqrt(hsq);
-              nm1 = d[4];
-              if (h < kBreakdownTol * beta) {
-                broke = true;
-                keep = j + 1;
-                hnext = 0.0;
-                break;
-              }
-              if (j + 1 < m_eff) {
-                if (lead) Wk.H[(j + 1) * ld + j] = h;
-                hcur = h;
-                h1 = h1n;
-                h2 = h2n;
-              } else {
-                hnext = h;
-                vnext_z = zout;
-                vnext_h1 = h1n;
-                vnext_h2 = h2n;
-                vnext_m1 = vm1;
-                vnext_v = vj;
-                vnext_expl = expl;
-              }
-            }
+            KrylovState ks = krylov_tiled(grid, sm, op, Wk, wp, beta, m_eff, mv);
+            keep = ks.keep;
+            broke = ks.broke;
+            hnext = ks.hnext;
+            vnext_z = ks.vz;
+            vnext_h1 = ks.h1;
+            vnext_h2 = ks.h2;
+            vnext_m1 = ks.vm1;
+            vnext_v = ks.vv;
+            vnext_expl = ks.expl;
           }
         }
         for (int64_t j = 0; j < m_eff && !tiled_done; ++j) {
@@ -1027,12 +1474,19 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
             hnext = h;
           }
         }
+        pc.mark(PC_KRYLOV);
         // ---- dense phi via the augmented exponential (kernels.py:148-193)
         __threadfence();
         grid.sync();
         if (blockIdx.x == 0) {
           const int dim = (int)(keep + p + 1);
-          double* M0 = Wk.scr;
+          const DenseSmem ds = dense_smem(Wk.dsm_bytes);
+          const bool in_smem = ds.n >= 6 * dim * dim;
+          double* Mq[6];
+          for (int q = 0; q < 6; ++q)
+            Mq[q] = in_smem ? ds.p + (int64_t)q * dim * dim : Wk.scr + (int64_t)q * MAXDIM * MAXDIM;
+          const DenseSmem dsx = in_smem ? DenseSmem{nullptr, 0} : ds;
+          double* M0 = Mq[0];
           for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) {
             const int i = idx / dim, jj = idx - i * dim;
             double hv = 0.0;
@@ -1045,8 +1499,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
           const double nrm_hat = blk_norm1(sm, M0, dim);
           for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) M0[idx] = tau * M0[idx];
           __syncthreads();
-          const int e = blk_expm(sm, Wk.scr, dim);
-          const double* E = Wk.scr + (int64_t)e * MAXDIM * MAXDIM;
+          const double* E = blk_expm(sm, Mq, dim, dsx);
           const double tp = pow(tau, (double)p);
           const int colp = p >= 1 ? (int)keep + p - 1 : 0;
           for (int i = threadIdx.x; i < keep; i += TPB) Wk.phi[i] = E[(int64_t)i * dim + colp] / tp;
@@ -1061,6 +1514,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         __syncthreads();
         corner = sm.phi[keep];
         nh = sm.phi[keep + 1];
+        pc.mark(PC_DENSE);
         eps = broke ? 0.0 : eik_mul(eik_mul(beta, fabs(hnext)), fabs(corner));
       }
 
@@ -1097,6 +1551,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         }
         grid_reduce<1>(grid, sm, r, Wk.part);
         const bool cand_nz = r[0] > 0.0;
+        pc.mark(PC_CAND);
 
         // ---- controller (phipm.py:336-359)
         const double omega = eik_div(eik_mul(t_out, eps), eik_mul(tau, T.tol));
@@ -1115,7 +1570,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         }
         const double tau_used = tau;
         Adapt ad = adapt_parameters(tau, m, t, eps, nh, t_out, T.rho[T.ns - 1], p,
-                                    T.tol, T.delta, T.m_max, n, Wk.nnz);
+                                    T.tol, T.delta, T.m_max, n, nnz);
         if (ok) {
           y = cand;
           ycur = ycur == 0 ? 1 : 0;

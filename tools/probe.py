@@ -23,5 +23,13 @@ for k in range(nsteps):
     mv = sum(c.matvecs for c in calls)
     print(f"step {k}: {ms:8.3f} ms device, wall {wall*1e3:8.2f} ms, matvecs {mv}, krylov {it}, "
           f"{ms/max(it,1)*1e3:7.1f} us/iter, calls {[ (c.substeps, c.rejections, c.matvecs, c.m_final) for c in calls]}", flush=True)
+import ctypes
+from paper_1805_02144_b200 import _native as nat
+pr = (ctypes.c_double * 16)()
+if nat.load().eik_prof_read(pr, 1) == 0:
+    names = ["rhs", "nnz", "wrec", "krylov", "dense", "cand", "dev", "misc"]
+    tot = sum(pr[:8])
+    print("phase share (CTA0 cycles, all steps):", ", ".join(f"{n} {100*pr[k]/tot:.1f}%" for k, n in enumerate(names)),
+          f"total {tot/1.965e6:.1f} ms")
 u = ctx.get_state()
 print("finite", np.isfinite(u).all(), "h range", u[3*ops.n_g:].min(), u[3*ops.n_g:].max())
