@@ -154,8 +154,12 @@ def context(ops):
     if ent is not None and ent[0]() is ops:
         return ent[1]
     ctx = SweContext(ops)
+    def _drop(_r, k=key, table=_CTX):
+        if table is not None:
+            table.pop(k, None)
+
     try:
-        ref = weakref.ref(ops, lambda _r, k=key: _CTX.pop(k, None))
+        ref = weakref.ref(ops, _drop)
     except TypeError:
         ref = (lambda o: (lambda: o))(ops)
     _CTX[key] = (ref, ctx)
