@@ -170,6 +170,9 @@ int64_t eik_swe_launches(const EikSwe* ctx);
 double eik_swe_last_kernel_ms(const EikSwe* ctx);
 /* Krylov iterations (IOM2 J*v) performed since creation */
 int64_t eik_swe_krylov_iters(const EikSwe* ctx);
+/* of those, iterations that needed the explicit orthogonalisation pass
+ * (Gram-identity norm rejected for cancellation) */
+int64_t eik_swe_explicit_orth(const EikSwe* ctx);
 
 /* ---------------------------------------------------------------- CSR */
 eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device,

@@ -83,6 +83,7 @@ _SIGS = {
     "eik_swe_launches": (C.c_int64, [_P]),
     "eik_swe_last_kernel_ms": (C.c_double, [_P]),
     "eik_swe_krylov_iters": (C.c_int64, [_P]),
+    "eik_swe_explicit_orth": (C.c_int64, [_P]),
     "eik_csr_create": (C.c_int, [C.c_int32, EikCsrView, C.c_int32, C.c_int32,
                                  C.POINTER(_P)]),
     "eik_csr_destroy": (C.c_int, [_P]),

@@ -1315,6 +1315,13 @@ int64_t eik_swe_krylov_iters(const EikSwe* c) {
   return (int64_t)v;
 }
 
+int64_t eik_swe_explicit_orth(const EikSwe* c) {
+  if (!c) return 0;
+  unsigned long long v[2] = {0, 0};
+  cudaMemcpy(v, c->eng.kiters_d, sizeof(v), cudaMemcpyDeviceToHost);
+  return (int64_t)v[1];
+}
+
 // ------------------------------------------------------------------ CSR
 eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max,
                           EikCsr** out) {

@@ -25,6 +25,7 @@ for k in range(nsteps):
           f"{ms/max(it,1)*1e3:7.1f} us/iter, calls {[ (c.substeps, c.rejections, c.matvecs, c.m_final) for c in calls]}", flush=True)
 import ctypes
 from paper_1805_02144_b200 import _native as nat
+print("explicit orthogonalisation passes:", nat.load().eik_swe_explicit_orth(ctx.h), "of", ctx.krylov_iters())
 pr = (ctypes.c_double * 16)()
 if nat.load().eik_prof_read(pr, 1) == 0:
     names = ["rhs", "nnz", "wrec", "krylov", "dense", "cand", "dev", "misc"]

@@ -1,0 +1,44 @@
+"""Copy a round's bench lines and ncu summaries into profiles/ (tracked)."""
+import csv, io, json, os, subprocess, sys
+from collections import defaultdict
+tag = sys.argv[1]
+src = "gpurun_out"
+dst = "profiles"
+os.makedirs(dst, exist_ok=True)
+for f in (f"bench_{tag}.json", f"bench_ref_{tag}.json"):
+    p = os.path.join(src, f)
+    if os.path.exists(p):
+        open(os.path.join(dst, f), "w").write(open(p).read())
+p = os.path.join(src, f"launches_{tag}.csv")
+if os.path.exists(p):
+    rows = list(csv.reader(open(p)))
+    k = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr, data = rows[k], rows[k + 1:]
+    ki, mi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in data:
+        if len(r) > mi:
+            name = r[ki].split("(")[0]
+            agg[name][0] += 1
+            agg[name][1] += float(r[mi].replace(",", ""))
+    tot = sum(v[1] for v in agg.values())
+    with open(os.path.join(dst, f"launches_{tag}.txt"), "w") as fh:
+        fh.write("ncu --metrics gpu__time_duration.sum --clock-control none "
+                 "(python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1); "
+                 "cold-cache serialised launches, compare shares\n")
+        for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            fh.write(f"{name:24s} launches={n:4d} total_ns={t:14.0f} share={100 * t / tot:6.2f}%\n")
+rep = os.path.join(src, f"step_{tag}.ncu-rep")
+if os.path.exists(rep):
+    out = subprocess.run([sys.executable, "tools/ncu_summary.py", rep], capture_output=True, text=True).stdout
+    r = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(io.StringIO(r.stdout)))
+    hdr = rows[0]
+    si, mi, ui, vi = (hdr.index(x) for x in ("Section Name", "Metric Name", "Metric Unit", "Metric Value"))
+    det = [f"{r[si][:30]:30s} {r[mi]:48s} {r[vi]:>16s} {r[ui]}" for r in rows[1:]
+           if r[si] in ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Occupancy",
+                        "Launch Statistics", "Warp State Statistics", "Compute Workload Analysis")]
+    with open(os.path.join(dst, f"ncu_full_k_swe_step_{tag}.txt"), "w") as fh:
+        fh.write(f"ncu --set full --clock-control none -k regex:k_swe_step -s 1 -c 1 "
+                 f"(one C3 L8 exprb42 step)\n\n{out}\n\n" + "\n".join(det) + "\n")
+print(sorted(os.listdir(dst)))
