@@ -262,7 +262,18 @@ def main():
     hbm, src = peaks()
     balg = b_alg_per_iter(ops)
     it_per_step = kiters / args.steps
-    achieved = balg * kiters / (dev_ms / 1e3) / 1e9
+    # algorithmic bytes of the step kernel's dominant work: every J*v pass
+    # (Krylov iterations and w-recurrence matvecs) at B_alg, plus the
+    # candidate update reading each kept basis vector once (32 B/cell)
+    step_bytes = balg * mv + 32.0 * ops.n_g * kiters
+    achieved = step_bytes / (dev_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            tr = json.load(fh)
+        if tr.get("cells") == ops.n_g:
+            traffic = tr["dram_bytes_per_jv"] * (mv / args.steps)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -279,10 +290,12 @@ def main():
         "krylov_iters_per_step": it_per_step, "matvecs_per_step": mv / args.steps,
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None,
-                     "note": f"kernel = whole-step k_swe_step; achieved = B_alg "
-                             f"({balg / 1e6:.1f} MB/iter, SURVEY §8d) x Krylov iters / "
-                             f"step-kernel time; peak {src}"},
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "note": f"kernel = whole-step k_swe_step (one launch per step); achieved "
+                             f"= (B_alg {balg / 1e6:.1f} MB x J*v passes + 32 B/cell x Krylov "
+                             f"iters) / step-kernel time, per launch; traffic = ncu DRAM "
+                             f"bytes per J*v pass (profiles/traffic.json) x J*v passes per "
+                             f"step; peak {src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * 4 * ops.n_g,
                 "d2h_bytes_per_step": 8 * 4 * ops.n_g},
         "gpu_launches": launches,

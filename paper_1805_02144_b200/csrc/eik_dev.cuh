@@ -346,6 +346,9 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
 #ifndef EIK_TMA
 #define EIK_TMA 0
 #endif
+#ifndef EIK_L2PF
+#define EIK_L2PF 0
+#endif
 // threads per own cell in the J v step (2: each thread does half the slots)
 #ifndef EIK_TPC
 #define EIK_TPC (EIK_TMA == 2 ? 2 : 1)
@@ -465,6 +468,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase)
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// Bulk L2 prefetch (sm_90+): pull a contiguous run into L2 without touching
+// registers or shared memory.
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  if (bytes >= 16)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u)
+                 : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -571,6 +581,29 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
 // the own cells -> epi(i, z, x_i).  A whole Krylov iteration (orthogonalise
 // + normalise v_j, L v_j, J v_j, projections) is one such pass: one HBM
 // sweep and one grid barrier per iteration.
+// Prefetch tile t's own-cell streams into L2 (the own cells are one
+// contiguous Hilbert range): the 54 compact-coefficient runs, the Laplacian
+// rows, (n, eta) and the vectors the pass reads.  Issued by warp 0 one tile
+// ahead so the DRAM stream keeps flowing while the current tile gathers.
+__device__ __forceinline__ void prefetch_tile(const SweOp& S, const Form& F, int t) {
+  if (t >= S.ntiles || threadIdx.x >= 32) return;
+  const int64_t c0 = __ldg(S.t_cell0 + t);
+  const int nT = __ldg(S.t_nT + t);
+  if (nT == 0) return;
+  const uint32_t run = (uint32_t)nT * 8;
+  for (int q = threadIdx.x; q < NCOEF + 7; q += 32) {
+    if (q < NCOEF) l2_prefetch(S.coefc + (int64_t)q * S.N + c0, run);
+    else if (q == NCOEF) l2_prefetch(S.Lc + c0 * 8, (uint32_t)nT * 64);
+    else if (q == NCOEF + 1) l2_prefetch(S.ne + c0, (uint32_t)nT * 32);
+    else if (q == NCOEF + 2) l2_prefetch(F.src + c0, (uint32_t)nT * 32);
+    else if (q == NCOEF + 3 && F.vm1) l2_prefetch(F.vm1 + c0, (uint32_t)nT * 32);
+    else if (q == NCOEF + 4 && F.vm2) l2_prefetch(F.vm2 + c0, (uint32_t)nT * 32);
+    else if (q == NCOEF + 5) l2_prefetch(S.lin + c0, (uint32_t)nT * 32);
+    else if (q == NCOEF + 6) l2_prefetch(S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8,
+                                         (uint32_t)__ldg(S.t_nE1 + t) * 16);
+  }
+}
+
 template <class Epi>
 __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
   const TileSmem ts = tile_smem(S);
@@ -585,7 +618,13 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
 #if EIK_PROF
   long long pt0 = clock64(), pt1, pacc[4] = {0, 0, 0, 0};
 #endif
+#if EIK_L2PF
+  prefetch_tile(S, F, blockIdx.x);
+#endif
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+#if EIK_L2PF
+    prefetch_tile(S, F, t + gridDim.x);
+#endif
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
     if (nT == 0) continue;  // uniform over the CTA
@@ -1101,7 +1140,8 @@ struct KrylovState {
 // H (row-major, leading dimension m_alloc) is written by CTA 0.
 __device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp& op,
                                     const EngineWork& Wk, const double4* wp, double beta,
-                                    int64_t m_eff, int64_t& mv) {
+                                    int64_t m_eff, int64_t& mv_out) {
+  int64_t mv = 0;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   const int64_t NU = Wk.NU, ld = Wk.m_alloc;
   int64_t lo, hi;
@@ -1195,6 +1235,7 @@ __device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp&
             out.expl = expl;
           }
         }
+  mv_out += mv;
   return out;
 }
 
@@ -1246,16 +1287,21 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
     tau0 = __ldcg(Wk.seeds + 2 * T.slot);
     m0 = (int64_t)__ldcg(Wk.seeds + 2 * T.slot + 1);
   }
-  double tau;
-  int64_t m;
-  initial_tau_m(tau0, m0, T.rho[0], T.rho[T.ns - 1], T.m_max, n, &tau, &m);
+  double tau_i;
+  int64_t m_i;
+  initial_tau_m(tau0, m0, T.rho[0], T.rho[T.ns - 1], T.m_max, n, &tau_i, &m_i);
   const int64_t m_cap = T.m_max < n ? T.m_max : n;
 
-  const double4* y = vnz[0] ? T.v[0] : Wk.zero;
-  bool y_nz = vnz[0];
-  int ycur = -1;
-  double t = 0.0;
-  int64_t attempts = 0, acc = 0, rej = 0, mv = 0;
+  // The engine's scalar state is kept in (L1-resident) local memory rather
+  // than registers: it is touched a few times per attempt, while the Krylov
+  // sweep in between needs every register for loads in flight.
+  volatile double tau = tau_i;
+  volatile int64_t m = m_i;
+  const double4* volatile y = vnz[0] ? T.v[0] : Wk.zero;
+  volatile bool y_nz = vnz[0];
+  volatile int ycur = -1;
+  volatile double t = 0.0;
+  volatile int64_t attempts = 0, acc = 0, rej = 0, mv = 0;
   const int64_t ld = Wk.m_alloc;
 
   for (int io = 0; io < T.ns; ++io) {
@@ -1376,7 +1422,9 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
             // on the fly from (z_{j-1}, v_{j-2}, v_{j-1}) with the previous
             // iteration's MGS coefficients, its norm taken from the Gram
             // identity (explicit pass only when that would cancel)
-            KrylovState ks = krylov_tiled(grid, sm, op, Wk, wp, beta, m_eff, mv);
+            int64_t kmv = 0;
+            KrylovState ks = krylov_tiled(grid, sm, op, Wk, wp, beta, m_eff, kmv);
+            mv += kmv;
             keep = ks.keep;
             broke = ks.broke;
             hnext = ks.hnext;
