@@ -129,6 +129,13 @@ eik_status eik_swe_jac_nnz(EikSwe* ctx, const double* u, int64_t* nnz);
 eik_status eik_swe_jac_nnz_rows(EikSwe* ctx, const double* u, int64_t* nnz,
                                 double* per_cell);
 
+/* conservation diagnostics (swe.py:226-237): out = {mass, energy, potential
+ * enstrophy}, each sum_i w_i q_i with w_i = weights[i] (per-cell areas) or
+ * cell_area when weights is NULL.  u NULL: the resident state (no host copy).
+ * EIK_EINVAL if some h <= 0. */
+eik_status eik_swe_diagnostics(EikSwe* ctx, const double* u, const double* weights,
+                               double cell_area, double* out);
+
 /* phipm_simul_iom2 with A x = dt * (J(u_lin) x).  W: n x ns, column-major
  * (column i contiguous).  trace may be NULL. */
 eik_status eik_swe_phipm(EikSwe* ctx, const double* u_lin, double dt,

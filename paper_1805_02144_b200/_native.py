@@ -66,6 +66,7 @@ _SIGS = {
     "eik_swe_jv": (C.c_int, [_P, _D, _D, _D]),
     "eik_swe_jac_nnz": (C.c_int, [_P, _D, C.POINTER(C.c_int64)]),
     "eik_swe_jac_nnz_rows": (C.c_int, [_P, _D, C.POINTER(C.c_int64), _D]),
+    "eik_swe_diagnostics": (C.c_int, [_P, _D, _D, C.c_double, _D]),
     "eik_swe_phipm": (C.c_int, [_P, _D, C.c_double, C.POINTER(EikPhiTask), _D,
                                 C.POINTER(EikPhipmInfo), C.POINTER(EikTraceRec),
                                 C.c_int64, C.POINTER(C.c_int64)]),

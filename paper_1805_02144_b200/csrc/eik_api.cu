@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -429,6 +430,41 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_kbench(SweArgs A) {
   set_status(A.status, EIK_OK);
 }
 
+
+// Conservation diagnostics (swe.py:226-237): weighted totals of mass h,
+// energy g h + |u|^2/2 and potential enstrophy (zeta + f)^2 / (2 h), with
+// zeta = V.u (no f: swe.py:233 subtracts it again).  Weights are per-cell
+// areas (A.dbg) or, when null, the scalar A.tol (reference: ops.cell_area).
+// Out: A.nnz_out[0..3] = mass, energy, enstrophy, count of h <= 0.
+__global__ void __launch_bounds__(TPB, MINB) k_swe_diag(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const SweOp& S = A.S1;
+  const double4* u = A.x;
+  int64_t lo, hi;
+  brange(S.N, lo, hi);
+  double r[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
+    double zeta = 0.0;
+    for (int s = 0; s < S.K; ++s) {
+      const double4 uj = u[S.nb(s, i)];
+      zeta += S.c(s, OP_VX, i) * uj.x + S.c(s, OP_VY, i) * uj.y + S.c(s, OP_VZ, i) * uj.z;
+    }
+    const double4 ui = u[i];
+    const double f = S.nf[i].w;
+    const double w = A.dbg ? A.dbg[i] : A.tol;
+    const double eta = zeta + f;
+    r[0] += w * ui.w;
+    r[1] += w * (S.g * ui.w + 0.5 * (ui.x * ui.x + ui.y * ui.y + ui.z * ui.z));
+    r[2] += w * (eta * eta / (2.0 * ui.w));
+    r[3] += (ui.w <= 0.0) ? 1.0 : 0.0;
+  }
+  grid_reduce<4>(grid, sm, r, A.Wk.part);
+  if (blockIdx.x == 0 && threadIdx.x < 4) A.nnz_out[threadIdx.x] = r[threadIdx.x];
+  set_status(A.status, EIK_OK);
+}
+
 struct CsrArgs {
   CsrOp C;
   EngineWork Wk;
@@ -515,9 +551,16 @@ struct EngineHost {
     n = n_;
     m_alloc = std::max<int64_t>(1, m_alloc_);
     smem = smem_bytes;
-    for (int k = 0; k < nk; ++k)
-      CK(cudaFuncSetAttribute(kernels[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(smem, 1)));
+    // the attribute is per function and process-wide: only ever raise it,
+    // so contexts with smaller tiles never break a larger one's launches
+    static std::map<const void*, size_t> attr_max;  // per kernel set
+    size_t& cur = attr_max[kernels[0]];
+    if (smem > cur) {
+      for (int k = 0; k < nk; ++k)
+        CK(cudaFuncSetAttribute(kernels[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+      cur = smem;
+    }
     G = coop_grid(kernels, nk, dev, NU, smem);
     wk.dsm_bytes = (int64_t)smem;
     if (G_override > 0) {
@@ -540,7 +583,7 @@ struct EngineHost {
     CK(mem.get(&info_d, 4));
     CK(mem.get(&trace_len_d, 1));
     CK(mem.get(&status_d, 1));
-    CK(mem.get(&nnz_d, 1));
+    CK(mem.get(&nnz_d, 4));
     CK(mem.get(&kiters_d, 4));
     wk.info = info_d;
     wk.trace = nullptr;
@@ -653,6 +696,7 @@ struct EikSwe {
           *vb = nullptr, *d2 = nullptr, *Ub = nullptr, *W[5] = {}, *x = nullptr,
           *out = nullptr;
   double* soa = nullptr;
+  double* wts = nullptr;  // diagnostics weights (lazily allocated)
   bool have_prev = false;
   double c09cube = 0.0;
   // graph cache for eik_swe_step
@@ -729,7 +773,8 @@ struct EikCsr {
 
 static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_rhs,
                                     (const void*)k_swe_jv, (const void*)k_swe_nnz,
-                                    (const void*)k_swe_phipm, (const void*)k_swe_kbench};
+                                    (const void*)k_swe_phipm, (const void*)k_swe_kbench,
+                                    (const void*)k_swe_diag};
 static const void* kCsrKernels[] = {(const void*)k_csr_phipm};
 
 extern "C" {
@@ -901,7 +946,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
   eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
-                             kSweKernels, 6, tile_smem_bytes(e1max, e2max, tma_ok), Gt);
+                             kSweKernels, 7, tile_smem_bytes(e1max, e2max, tma_ok), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
   int *d_nbr, *d_dfx, *d_cnt;
@@ -1273,6 +1318,39 @@ eik_status eik_swe_krylov_bench(EikSwe* c, const double* u, const double* v, dou
   CK(cudaMemcpy(&keep, c->eng.nnz_d, sizeof(double), cudaMemcpyDeviceToHost));
   out[0] = ms;
   out[1] = keep;
+  return EIK_OK;
+}
+
+
+eik_status eik_swe_diagnostics(EikSwe* c, const double* u, const double* weights,
+                               double cell_area, double* out) {
+  if (!c || !out) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  eik_status s = EIK_OK;
+  double4* src = c->u;
+  if (u) {
+    if ((s = c->h2d_cells(u, c->x)) != EIK_OK) return s;
+    src = c->x;
+  }
+  double* wdev = nullptr;
+  if (weights) {
+    if (!c->wts) CK(c->eng.mem.get(&c->wts, c->N));
+    CK(cudaMemcpyAsync(c->wts, weights, c->N * sizeof(double), cudaMemcpyHostToDevice,
+                       c->eng.st));
+    wdev = c->wts;
+  }
+  SweArgs A = c->args(src);
+  A.x = src;
+  A.dbg = wdev;
+  A.tol = cell_area;
+  if ((s = c->launch((const void*)k_swe_diag, A)) != EIK_OK) return s;
+  if ((s = c->status()) != EIK_OK) return s;
+  double v[4];
+  CK(cudaMemcpy(v, c->eng.nnz_d, sizeof(v), cudaMemcpyDeviceToHost));
+  if (v[3] > 0.0) return fail(EIK_EINVAL, "height field must be positive");
+  out[0] = v[0];
+  out[1] = v[1];
+  out[2] = v[2];
   return EIK_OK;
 }
 

@@ -11,6 +11,7 @@ resident trajectory state and the engine's warm-start seeds.
 
 import ctypes as C
 import weakref
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -170,6 +171,36 @@ def rhs(ops, state):
     """Tendency of [u_x; u_y; u_z; h] (swe.py:149-168), computed on the GPU.
     Raises ValueError on a non-finite state or tendency."""
     return context(ops).rhs(state)
+
+
+@dataclass
+class Diagnostics:
+    """Weighted conserved totals and drifts relative to t=0 (swe.py:49-62)."""
+
+    mass: float
+    energy: float
+    enstrophy: float
+
+    def drifts(self, initial):
+        return ((self.mass - initial.mass) / initial.mass,
+                (self.energy - initial.energy) / initial.energy,
+                (self.enstrophy - initial.enstrophy) / initial.enstrophy)
+
+
+def diagnostics(ops, state=None, area_weighted=False):
+    """Totals of mass (h), energy (g h + |u|^2/2) and potential enstrophy
+    ((zeta+f)^2 / 2h) on the GPU (swe.py:226-237).  The reference weights
+    every cell by the scalar ``ops.cell_area``; ``area_weighted=True`` uses
+    the sphere grid's per-cell areas.  ``state=None`` reads the context's
+    resident trajectory state without a host copy."""
+    ctx = context(ops)
+    out = np.zeros(3)
+    u = None if state is None else ctx._vec(state)
+    w = np.ascontiguousarray(ops.areas, dtype=float) if area_weighted else None
+    nat.check(nat.load().eik_swe_diagnostics(
+        ctx.h, None if u is None else nat.dptr(u), None if w is None else nat.dptr(w),
+        float(ops.cell_area), nat.dptr(out)), "diagnostics")
+    return Diagnostics(mass=float(out[0]), energy=float(out[1]), enstrophy=float(out[2]))
 
 
 class SweJacobian(DeviceOperator):

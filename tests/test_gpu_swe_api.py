@@ -95,3 +95,42 @@ def test_rhs_on_planar_reference_style_operators():
     assert np.linalg.norm(gswe.assemble_jacobian(ops, u).matvec(v) - J.matvec(v)) <= \
         1e-12 * np.linalg.norm(J.matvec(v))
     assert gswe.jacobian_nnz(ops, u) == J.nnz
+
+
+def test_diagnostics_match_reference_formula(c0):
+    """swe.py:226-237 restated: mass/energy/enstrophy with the scalar
+    cell_area, and the per-cell-area variant."""
+    ops, u0, _ = c0
+    N = ops.n_g
+    ux, uy, uz, h = np.split(u0, 4)
+    zeta = ops.Vx.csr @ ux + ops.Vy.csr @ uy + ops.Vz.csr @ uz
+    for weighted in (False, True):
+        w = ops.areas if weighted else np.full(N, ops.cell_area)
+        mass = np.sum(w * h)
+        energy = np.sum(w * (ops.g * h + 0.5 * (ux * ux + uy * uy + uz * uz)))
+        ens = np.sum(w * (zeta + ops.f) ** 2 / (2.0 * h))
+        d = gswe.diagnostics(ops, u0, area_weighted=weighted)
+        assert abs(d.mass - mass) <= 1e-13 * mass
+        assert abs(d.energy - energy) <= 1e-13 * energy
+        assert abs(d.enstrophy - ens) <= 1e-12 * ens
+    bad = u0.copy()
+    bad[3 * N + 5] = -1.0
+    with pytest.raises(ValueError):
+        gswe.diagnostics(ops, bad)
+
+
+def test_mass_conserved_by_steps(c0):
+    """Flux-form divergence: area-weighted mass is conserved to rounding by
+    every scheme over several steps (acceptance criterion 8 analogue,
+    test_acceptance.py:154-168), measured on the resident state."""
+    ops, u0, spec = c0
+    ctx = gswe.SweContext(ops)
+    ctx.set_state(u0)
+    d0 = gswe.diagnostics(ops, u0, area_weighted=True)
+    for k in range(6):
+        ctx.step("exprb42", spec.dt, spec.tol)
+    u = ctx.get_state()
+    d = gswe.diagnostics(ops, u, area_weighted=True)
+    dm, de, dz = d.drifts(d0)
+    assert abs(dm) <= 1e-12
+    assert abs(de) <= 1e-3 and abs(dz) <= 1e-2
