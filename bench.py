@@ -231,13 +231,9 @@ def main():
     clocks = clk.stop()
     launches = ctx.launches() - l0
     kiters = ctx.krylov_iters() - k0
-    ms = dev_ms
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    from paper_1805_02144_b200.replicas import aggregate_throughput, max_over_ranks
+    value, ms = aggregate_throughput(args.steps, dev_ms, dist, f"cuda:{local}")
     ms_per_step = ms / args.steps
-    value = ws * args.steps / (ms / 1e3)
 
     # end to end through the C ABI: pinned host state in, step, state out
     pin_in = torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory()
@@ -253,11 +249,7 @@ def main():
         nat.check(nat.load().eik_swe_get_state(ctx.h, nat.dptr(hout)), "get_state")
         hin[:] = hout
     e2e_wall = time.perf_counter() - te
-    e2e = ws * args.e2e_steps / e2e_wall
-    if dist:
-        t = torch.tensor([e2e_wall], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = ws * args.e2e_steps / float(t.item())
+    e2e, _ = aggregate_throughput(args.e2e_steps, 1e3 * e2e_wall, dist, f"cuda:{local}")
 
     hbm, src = peaks()
     balg = b_alg_per_iter(ops)
