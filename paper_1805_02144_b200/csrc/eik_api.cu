@@ -345,7 +345,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
         st = EIK_EINVAL;
     }
     if (st != EIK_OK) break;
-    st = engine_call(grid, sm, A.SD, T, A.Wk, nA);
+    // the task lives in shared memory during the call: its fields are read a
+    // few times per attempt and must not occupy registers across the sweep
+    __shared__ EngineTask sT;
+    if (threadIdx.x == 0) sT = T;
+    __syncthreads();
+    st = engine_call(grid, sm, A.SD, sT, A.Wk, nA);
     pc.skip();
   }
   if (st == EIK_OK) {
@@ -561,10 +566,11 @@ struct EngineHost {
                                 (int)smem));
       cur = smem;
     }
+    const int cap = coop_grid(kernels, nk, dev, 1LL << 40, smem);  // co-resident capacity
     G = coop_grid(kernels, nk, dev, NU, smem);
     wk.dsm_bytes = (int64_t)smem;
     if (G_override > 0) {
-      if (G_override > G)
+      if (G_override > cap)
         return fail(EIK_ECUDA, "cooperative grid does not fit the device");
       G = G_override;
     }
@@ -1176,8 +1182,11 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
   A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
   A.Wk.trace_cap = (trace && trace_cap > 0) ? trace_cap : 0;
   CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
+  CK(cudaEventRecord(c->ev0, E.st));
   if ((s = c->launch((const void*)k_swe_phipm, A)) != EIK_OK) return s;
+  CK(cudaEventRecord(c->ev1, E.st));
   s = E.finish_phipm(info, trace, trace_cap, trace_len);
+  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
   if (s != EIK_OK) return s;
   for (int i = 0; i < task->ns; ++i)
     if ((s = c->d2h_cells(E.wout[i], W + (size_t)i * 4 * c->N)) != EIK_OK) return s;

@@ -26,10 +26,10 @@ namespace cg = cooperative_groups;
 namespace eik {
 
 #ifndef EIK_TPB
-#define EIK_TPB 256
+#define EIK_TPB 512
 #endif
 #ifndef EIK_MINB
-#define EIK_MINB 2
+#define EIK_MINB 1
 #endif
 constexpr int TPB = EIK_TPB;    // threads per CTA
 constexpr int MINB = EIK_MINB;  // co-resident CTAs per SM (register budget)
@@ -354,7 +354,22 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
 #define EIK_TPC (EIK_TMA == 2 ? 2 : 1)
 #endif
 constexpr int TPC = EIK_TPC;
-constexpr int TILE = TPB / TPC;  // max own cells per tile
+// EIK_WS: warp-specialised tiled pass -- the first half of the CTA gathers
+// and stages tile k+1 (steps 1-2) while the second half computes J x on
+// tile k (step 3); two shared-memory tile buffers, named barriers.
+#ifndef EIK_WS
+#define EIK_WS (EIK_TPB == 512 && EIK_TMA == 0)
+#endif
+constexpr int WS = EIK_WS;
+#ifndef EIK_PT
+#define EIK_PT (EIK_TPB / 2)
+#endif
+#ifndef EIK_WS_TPC
+#define EIK_WS_TPC 1
+#endif
+constexpr int PT = EIK_PT;                       // producer threads (WS)
+constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell (WS)
+constexpr int TILE = WS ? (TPB - PT) / WS_TPC : TPB / TPC;  // max own cells per tile
 #ifndef EIK_PROF
 #define EIK_PROF 0
 #endif
@@ -406,11 +421,15 @@ __host__ __device__ constexpr size_t tile_tma_bytes(int tma) {
                         (tma == 2 ? (size_t)TILE * (32 + 16 + 64) : 0);
 }
 
-__device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
+__host__ __device__ constexpr size_t tile_buf_bytes(int e1max, int e2max) {
+  return (size_t)e2max * 32 + (size_t)e1max * 64 + (size_t)e2max * 4 + 16;
+}
+
+__device__ __forceinline__ TileSmem tile_smem(const SweOp& S, int buf = 0) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TileSmem t;
   t.bar = reinterpret_cast<unsigned long long*>(dsm);
-  unsigned char* p = dsm + 128;
+  unsigned char* p = dsm + 128 + (size_t)buf * ((tile_buf_bytes(S.e1max, S.e2max) + 127) / 128 * 128);
   t.cb = reinterpret_cast<double*>(p);
   unsigned char* p2 = p + (size_t)NCOEF * TILE * 8;
   t.neb = reinterpret_cast<double4*>(p2);
@@ -433,8 +452,9 @@ __device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
 }
 
 __host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max, int tma) {
-  return 128 + tile_tma_bytes(tma) + (size_t)e2max * 32 + (size_t)e1max * 64 +
-         (size_t)e2max * 4 + 16;
+  return 128 + tile_tma_bytes(tma) +
+         (WS ? 2 * ((tile_buf_bytes(e1max, e2max) + 127) / 128 * 128)
+             : tile_buf_bytes(e1max, e2max));
 }
 
 // ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
@@ -495,6 +515,13 @@ struct JvAcc {
   double zeta, gx, gy, gz, dv, l0, l1, l2, l3;
 };
 
+#ifndef EIK_CHUNK
+#define EIK_CHUNK 3
+#endif
+// Slots are processed in chunks of EIK_CHUNK: all 9*CHUNK coefficient loads
+// of a chunk are issued before any of them is used (a compiler memory fence
+// keeps them together), so each thread keeps ~27 streaming loads in flight
+// instead of the handful the default schedule interleaves with the math.
 template <int kSrc, int NS>
 __device__ __forceinline__ JvAcc swe_jv_part(const SweOp& S, const TileSmem& ts, const short* row,
                                              const double* lc, int s0, int c, int64_t i,
@@ -505,37 +532,47 @@ __device__ __forceinline__ JvAcc swe_jv_part(const SweOp& S, const TileSmem& ts,
                fzi = Ui.w * ai.z + Ui.z * ai.w;
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t st = (int64_t)9 * S.N;
+  constexpr int CH = (EIK_CHUNK < NS) ? EIK_CHUNK : NS;
 #pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    const int s = s0 + k;
-    const int l = row[s];
-    double vx, vy, vz, gcx, gcy, gcz, dx, dy, dz;
-    if constexpr (kSrc == 1) {
-      const double* cp = ts.cb + (s * 9) * TILE + c;
-      vx = cp[0]; vy = cp[TILE]; vz = cp[2 * TILE];
-      gcx = cp[3 * TILE]; gcy = cp[4 * TILE]; gcz = cp[5 * TILE];
-      dx = cp[6 * TILE]; dy = cp[7 * TILE]; dz = cp[8 * TILE];
-    } else {
-      const double* cp = S.coefc + i + s * st;
-      vx = __ldcs(cp); vy = __ldcs(cp + S.N); vz = __ldcs(cp + 2 * S.N);
-      gcx = __ldcs(cp + 3 * S.N); gcy = __ldcs(cp + 4 * S.N); gcz = __ldcs(cp + 5 * S.N);
-      dx = __ldcs(cp + 6 * S.N); dy = __ldcs(cp + 7 * S.N); dz = __ldcs(cp + 8 * S.N);
+  for (int k0 = 0; k0 < NS; k0 += CH) {
+    double cf[CH][9];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int s = s0 + k0 + k;
+      if constexpr (kSrc == 1) {
+        const double* cp = ts.cb + (s * 9) * TILE + c;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cf[k][q] = cp[q * TILE];
+      } else {
+        const double* cp = S.coefc + i + s * st;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cf[k][q] = __ldcs(cp + q * S.N);
+      }
     }
-    const double l0 = lc[s];
-    const double4 aj = sld(ts.x, l);
-    const double4 U = sld(ts.U, l);
-    const double4 la = sld(ts.La, l);
-    a.zeta += vx * (aj.x - ai.x) + vy * (aj.y - ai.y) + vz * (aj.z - ai.z);
-    const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
-    a.gx += gcx * (e - ei);
-    a.gy += gcy * (e - ei);
-    a.gz += gcz * (e - ei);
-    a.dv += dx * ((U.w * aj.x + U.x * aj.w) + fxi) + dy * ((U.w * aj.y + U.y * aj.w) + fyi) +
-            dz * ((U.w * aj.z + U.z * aj.w) + fzi);
-    a.l0 += l0 * (la.x - lai.x);
-    a.l1 += l0 * (la.y - lai.y);
-    a.l2 += l0 * (la.z - lai.z);
-    a.l3 += l0 * (la.w - lai.w);
+    if constexpr (kSrc == 0) asm volatile("" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int s = s0 + k0 + k;
+      const int l = row[s];
+      const double vx = cf[k][0], vy = cf[k][1], vz = cf[k][2];
+      const double gcx = cf[k][3], gcy = cf[k][4], gcz = cf[k][5];
+      const double dx = cf[k][6], dy = cf[k][7], dz = cf[k][8];
+      const double l0 = lc[s];
+      const double4 aj = sld(ts.x, l);
+      const double4 U = sld(ts.U, l);
+      const double4 la = sld(ts.La, l);
+      a.zeta += vx * (aj.x - ai.x) + vy * (aj.y - ai.y) + vz * (aj.z - ai.z);
+      const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
+      a.gx += gcx * (e - ei);
+      a.gy += gcy * (e - ei);
+      a.gz += gcz * (e - ei);
+      a.dv += dx * ((U.w * aj.x + U.x * aj.w) + fxi) + dy * ((U.w * aj.y + U.y * aj.w) + fyi) +
+              dz * ((U.w * aj.z + U.z * aj.w) + fzi);
+      a.l0 += l0 * (la.x - lai.x);
+      a.l1 += l0 * (la.y - lai.y);
+      a.l2 += l0 * (la.z - lai.z);
+      a.l3 += l0 * (la.w - lai.w);
+    }
   }
   return a;
 }
@@ -604,8 +641,161 @@ __device__ __forceinline__ void prefetch_tile(const SweOp& S, const Form& F, int
   }
 }
 
+
+// ---- warp-specialised pipeline (EIK_WS) --------------------------------
+__device__ __forceinline__ void nb_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// named barrier ids: 1 producer-internal, 2+b FULL[b], 4+b EMPTY[b]
+template <class Epi>
+__device__ void swe_tiled_ws(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
+  constexpr int HALF = PT;  // producer threads
+  const bool prod = threadIdx.x < HALF;
+  const int lt = prod ? threadIdx.x : threadIdx.x - HALF;
+  int ktiles = 0;
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) ++ktiles;
+#if EIK_PROF
+  long long wt = 0, t0p = clock64();
+#endif
+  if (prod) {
+    for (int k = 0; k < ktiles; ++k) {
+      const int t = blockIdx.x + k * gridDim.x;
+      const int b = k & 1;
+      const TileSmem ts = tile_smem(S, b);
+#if EIK_PROF
+      long long w0 = clock64();
+#endif
+      if (k >= 2) nb_sync(4 + b, TPB);  // consumer released buffer b
+#if EIK_PROF
+      wt += clock64() - w0;
+#endif
+      const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+      const int* map = S.e2map + __ldg(S.t_e2off + t);
+      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+      for (int base = 0; base < nE2; base += 2 * HALF) {
+        const int ca = base + lt, cb = ca + HALF;
+        const bool va = ca < nE2, vb = cb < nE2;
+        const int ga = va ? __ldg(map + ca) : 0;
+        const int gb = vb ? __ldg(map + cb) : 0;
+        double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
+                b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
+        if (va) {
+          a0 = F.src[ga];
+          if (F.vm2) a1 = F.vm2[ga];
+          if (F.vm1) a2 = F.vm1[ga];
+          if (ca < nE1) ua = S.lin[ga];
+        }
+        if (vb) {
+          b0 = F.src[gb];
+          if (F.vm2) b1 = F.vm2[gb];
+          if (F.vm1) b2 = F.vm1[gb];
+          if (cb < nE1) ub = S.lin[gb];
+        }
+        if (va) {
+          const double4 x = form_x(F, a0, a1, a2);
+          ts.gid[ca] = ga;
+          sst(ts.x, ca, x);
+          if (ca < nE1) sst(ts.U, ca, ua);
+          if (F.out && ca < nT) F.out[ga] = x;
+        }
+        if (vb) {
+          const double4 x = form_x(F, b0, b1, b2);
+          ts.gid[cb] = gb;
+          sst(ts.x, cb, x);
+          if (cb < nE1) sst(ts.U, cb, ub);
+          if (F.out && cb < nT) F.out[gb] = x;
+        }
+      }
+      nb_sync(1, HALF);
+      for (int c = lt; c < nE1; c += HALF) {
+        const Row8 row = load_row8(rows + (int64_t)c * 8);
+        const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
+        const double4 xc = sld(ts.x, c);
+        double4 acc = d4(0.0);
+#pragma unroll
+        for (int s = 0; s < KCMAX; ++s) {
+          const double l = __ldg(lc + s);
+          const double4 xv = sld(ts.x, row.s[s]);
+          acc.x += l * (xv.x - xc.x);
+          acc.y += l * (xv.y - xc.y);
+          acc.z += l * (xv.z - xc.z);
+          acc.w += l * (xv.w - xc.w);
+        }
+        sst(ts.La, c, acc);
+      }
+      nb_arrive(2 + b, TPB);  // buffer b full
+    }
+    // drain the consumer's last releases so the barriers start clean next time
+    for (int k = ktiles > 2 ? ktiles - 2 : 0; k < ktiles; ++k) nb_sync(4 + (k & 1), TPB);
+  } else {
+    for (int k = 0; k < ktiles; ++k) {
+      const int t = blockIdx.x + k * gridDim.x;
+      const int b = k & 1;
+      const TileSmem ts = tile_smem(S, b);
+#if EIK_PROF
+      long long w0 = clock64();
+#endif
+      nb_sync(2 + b, TPB);  // wait for buffer b
+#if EIK_PROF
+      wt += clock64() - w0;
+#endif
+      const int64_t c0 = __ldg(S.t_cell0 + t);
+      const int nT = __ldg(S.t_nT + t);
+      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+      {
+        const int c0l = lt / WS_TPC, part = lt % WS_TPC;
+        const bool live = c0l < nT;
+        const int c = live ? c0l : 0;
+        const int64_t i = c0 + c;
+        const double4 ai = sld(ts.x, c);
+        const double4 Ui = sld(ts.U, c);
+        const double4 lai = sld(ts.La, c);
+        const Row8 row = load_row8(rows + (int64_t)c * 8);
+        const double* lc = S.Lc + i * 8;
+        double lcr[8];
+#pragma unroll
+        for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
+        JvAcc a = swe_jv_part<0, KCMAX / WS_TPC>(S, ts, row.s, lcr, part * (KCMAX / WS_TPC), c,
+                                                  i, ai, Ui, lai);
+        if constexpr (WS_TPC == 2) {
+          a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
+          a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
+          a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
+          a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
+          a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
+          a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
+          a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
+          a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
+          a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
+        }
+        if (live && part == 0) {
+          const double4 z = S.scale * swe_jv_finish(S, a, S.ne[i], ai, Ui);
+          const double4 vm = F.epi_vm1 ? F.epi_vm1[i] : d4(0.0);
+          epi(i, z, ai, vm);
+        }
+      }
+      nb_arrive(4 + b, TPB);  // buffer b free
+    }
+  }
+#if EIK_PROF
+  if (S.prof && (threadIdx.x == 0 || threadIdx.x == PT)) {
+    const int o = threadIdx.x == 0 ? 0 : 2;
+    atomicAdd(S.prof + o, (unsigned long long)wt);                       // wait
+    atomicAdd(S.prof + o + 1, (unsigned long long)(clock64() - t0p));    // total
+  }
+#endif
+  __syncthreads();
+}
+
 template <class Epi>
 __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
+  if constexpr (WS) {
+    swe_tiled_ws(sm, S, F, epi);
+    return;
+  }
   const TileSmem ts = tile_smem(S);
   const int tma = S.tma;
   if (tma && threadIdx.x == 0 && !sm.bar_init) {
@@ -621,12 +811,31 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
 #if EIK_L2PF
   prefetch_tile(S, F, blockIdx.x);
 #endif
+  // the first round of step 1 uses local->global indices fetched one tile
+  // ahead (they are loaded while the previous tile's steps 2-3 run)
+  int pga = 0, pgb = 0;
+  if (blockIdx.x < S.ntiles) {
+    const int* m0 = S.e2map + __ldg(S.t_e2off + blockIdx.x);
+    const int n0 = __ldg(S.t_nE2 + blockIdx.x);
+    if ((int)threadIdx.x < n0) pga = __ldg(m0 + threadIdx.x);
+    if ((int)threadIdx.x + TPB < n0) pgb = __ldg(m0 + threadIdx.x + TPB);
+  }
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
 #if EIK_L2PF
     prefetch_tile(S, F, t + gridDim.x);
 #endif
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+    const int cur_ga = pga, cur_gb = pgb;
+    {
+      const int tn = t + gridDim.x;
+      if (tn < S.ntiles) {
+        const int* mn = S.e2map + __ldg(S.t_e2off + tn);
+        const int nn = __ldg(S.t_nE2 + tn);
+        pga = ((int)threadIdx.x < nn) ? __ldg(mn + threadIdx.x) : 0;
+        pgb = ((int)threadIdx.x + TPB < nn) ? __ldg(mn + threadIdx.x + TPB) : 0;
+      }
+    }
     if (nT == 0) continue;  // uniform over the CTA
     const int* map = S.e2map + __ldg(S.t_e2off + t);
     const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
@@ -654,11 +863,14 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       if (tma == 1 && threadIdx.x == 0) tma_g2s(ts.neb, S.ne + c0, (uint32_t)nT * 32, ts.bar + 1);
     }
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
-    for (int base = 0; base < nE2; base += 2 * TPB) {
+#ifndef EIK_ABL
+#define EIK_ABL 0
+#endif
+    for (int base = 0; base < ((EIK_ABL & 1) ? 0 : nE2); base += 2 * TPB) {
       const int ca = base + threadIdx.x, cb = ca + TPB;
       const bool va = ca < nE2, vb = cb < nE2;
-      const int ga = va ? __ldg(map + ca) : 0;
-      const int gb = vb ? __ldg(map + cb) : 0;
+      const int ga = !va ? 0 : (base == 0 ? cur_ga : __ldg(map + ca));
+      const int gb = !vb ? 0 : (base == 0 ? cur_gb : __ldg(map + cb));
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
               b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
       if (va) {
@@ -694,7 +906,7 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
     pt1 = clock64(); pacc[0] += pt1 - pt0; pt0 = pt1;
 #endif
     // step 2: L x on E1 (difference form)
-    for (int c = threadIdx.x; c < nE1; c += TPB) {
+    for (int c = threadIdx.x; c < ((EIK_ABL & 2) ? 0 : nE1); c += TPB) {
       const bool own2 = (tma == 2) && c < nT;
       const Row8 row = own2 ? *reinterpret_cast<const Row8*>(ts.rowb + c * 8)
                             : load_row8(rows + (int64_t)c * 8);
@@ -719,7 +931,7 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
     // step 3: z = scale * J x on the own cells (TPC threads per cell)
     if (tma) mbar_wait(ts.bar + 1, ph);
     ph ^= 1u;
-    {
+    if (!(EIK_ABL & 4)) {
       const int c = threadIdx.x / TPC;
       const int part = threadIdx.x % TPC;
       const bool live = c < nT;
@@ -756,7 +968,7 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
         a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
         a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
       }
-      if (live && part == 0) {
+      if (live && part == 0 && !(EIK_ABL & 4)) {
         const double4 q = tma ? ts.neb[cc] : S.ne[i];
         const double4 z = S.scale * swe_jv_finish(S, a, q, ai, Ui);
         const double4 vm = F.epi_vm1 ? (tma == 2 ? ts.vmb[cc] : F.epi_vm1[i]) : d4(0.0);

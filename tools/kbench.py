@@ -23,7 +23,10 @@ us = out[0] * 1e3 / it
 print(f"{name} N={N} m={m} reps={reps}: {out[0]:.3f} ms total, {us:.1f} us/iter, keep {out[1]}, "
       f"B_alg {balg/1e6:.1f} MB -> {balg/us/1e3:.0f} GB/s ({balg/us/1e3/6543.4*100:.1f}% of 6543.4)")
 nat.check(nat.load().eik_swe_info(ctx.h, info))
-if info[12]:
+if info[10] and info[12] and len(sys.argv) > 4 and sys.argv[4] == "ws":
+    print("WS: producer wait %.1f%% of its time, consumer wait %.1f%% of its time" % (
+        100 * info[9] / info[10], 100 * info[11] / info[12]))
+elif info[12]:
     tot = info[9] + info[10] + info[11]
     print("tile step cycles share: step1 %.1f%% step2 %.1f%% step3 %.1f%%, per-CTA-call avg %.0f us" % (
         100 * info[9] / tot, 100 * info[10] / tot, 100 * info[11] / tot, tot / info[12] / 1965.0))
