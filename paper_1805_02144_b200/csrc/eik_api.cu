@@ -1062,7 +1062,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.prof = nullptr;
   if (EIK_PROF) {
     unsigned long long* pr;
-    if (B.get(&pr, 4) == cudaSuccess) S.prof = pr;
+    if (B.get(&pr, 8) == cudaSuccess) S.prof = pr;
   }
   S.e1max = e1max;
   S.e2max = e2max;
@@ -1375,9 +1375,9 @@ eik_status eik_swe_info(const EikSwe* c, int64_t* out) {
   out[7] = c->S.tiled_ok;
   out[8] = (int64_t)c->eng.smem;
   if (c->S.prof) {
-    unsigned long long pv[4];
+    unsigned long long pv[5];
     cudaMemcpy(pv, c->S.prof, sizeof(pv), cudaMemcpyDeviceToHost);
-    for (int k = 0; k < 4; ++k) out[9 + k] = (int64_t)pv[k];
+    for (int k = 0; k < 5; ++k) out[9 + k] = (int64_t)pv[k];
   }
   return EIK_OK;
 }

@@ -358,7 +358,7 @@ constexpr int TPC = EIK_TPC;
 // and stages tile k+1 (steps 1-2) while the second half computes J x on
 // tile k (step 3); two shared-memory tile buffers, named barriers.
 #ifndef EIK_WS
-#define EIK_WS (EIK_TPB == 512 && EIK_TMA == 0)
+#define EIK_WS ((EIK_TPB == 512 && EIK_TMA == 0) ? 2 : 0)
 #endif
 constexpr int WS = EIK_WS;
 #ifndef EIK_PT
@@ -370,6 +370,7 @@ constexpr int WS = EIK_WS;
 constexpr int PT = EIK_PT;                       // producer threads (WS)
 constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell (WS)
 constexpr int TILE = WS ? (TPB - PT) / WS_TPC : TPB / TPC;  // max own cells per tile
+static_assert(WS != 2 || TILE == 256, "TMA-WS: 256-cell tiles");
 #ifndef EIK_PROF
 #define EIK_PROF 0
 #endif
@@ -451,7 +452,12 @@ __device__ __forceinline__ TileSmem tile_smem(const SweOp& S, int buf = 0) {
   return t;
 }
 
+__host__ __device__ constexpr size_t tw_buf_bytes(int e1max, int e2max) {
+  return ((size_t)e2max * 32 + (size_t)e1max * 64 + 127) / 128 * 128;
+}
 __host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max, int tma) {
+  if (WS == 2)
+    return 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 + 2 * tw_buf_bytes(e1max, e2max);
   return 128 + tile_tma_bytes(tma) +
          (WS ? 2 * ((tile_buf_bytes(e1max, e2max) + 127) / 128 * 128)
              : tile_buf_bytes(e1max, e2max));
@@ -790,9 +796,290 @@ __device__ void swe_tiled_ws(Smem& sm, const SweOp& S, const Form& F, const Epi&
   __syncthreads();
 }
 
+
+// ---- TMA warp-specialised pipeline (EIK_WS == 2) ---------------------------
+// warp 0: TMA issuer -- streams each tile's own-cell coefficients (54 runs,
+//         two halves of 3 stencil slots) and (n, eta) into shared memory
+//         through cp.async.bulk + mbarriers, one half ahead of the consumers;
+// warps 1..PT/32-1: gatherers -- steps 1-2 of tile k+1 (x on E2, L x on E1)
+//         into tile buffer (k+1)&1;
+// warps PT/32..: consumers -- step 3 (J x) from shared memory only.
+struct TwSmem {
+  unsigned long long* cfull;   // [2] coefficient half h landed (tx-count)
+  unsigned long long* cempty;  // [2] consumers released half h (8 warp arrivals)
+  double* cb;                  // [NCOEF][TILE]
+  double4* neb;                // [TILE]
+  SArr x, La, U;               // tile buffer
+};
+__device__ __forceinline__ TwSmem tw_smem(const SweOp& S, int buf) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  TwSmem t;
+  t.cfull = reinterpret_cast<unsigned long long*>(dsm);
+  t.cempty = t.cfull + 2;
+  t.cb = reinterpret_cast<double*>(dsm + 128);
+  t.neb = reinterpret_cast<double4*>(dsm + 128 + (size_t)NCOEF * TILE * 8);
+  unsigned char* p = dsm + 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
+                     (size_t)buf * tw_buf_bytes(S.e1max, S.e2max);
+  double2* q = reinterpret_cast<double2*>(p);
+  t.x = SArr{q, S.e2max};
+  q += 2 * S.e2max;
+  t.La = SArr{q, S.e1max};
+  q += 2 * S.e1max;
+  t.U = SArr{q, S.e1max};
+  return t;
+}
+__device__ __forceinline__ TileSmem ts_as_tile(const TwSmem& b, const TwSmem& t0) {
+  TileSmem r;
+  r.bar = nullptr;
+  r.cb = t0.cb;
+  r.neb = t0.neb;
+  r.vmb = nullptr;
+  r.rowb = nullptr;
+  r.lcb = nullptr;
+  r.x = b.x;
+  r.La = b.La;
+  r.U = b.U;
+  r.gid = nullptr;
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive1(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <class Epi>
+__device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
+  constexpr int GT = PT - 32;            // gatherer threads
+  constexpr int CT = TPB - PT;           // consumer threads (== TILE * WS_TPC)
+  constexpr int NB = GT + CT;            // named-barrier participants
+  constexpr int NCW = CT / 32;           // consumer warps
+  constexpr int HALF_RUNS = NCOEF / 2;   // 27 runs per half (3 slots x 9 ops)
+  const int warp = threadIdx.x >> 5;
+  const TwSmem t0 = tw_smem(S, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(t0.cfull, 1);
+    mbar_init(t0.cfull + 1, 1);
+    mbar_init(t0.cempty, NCW);
+    mbar_init(t0.cempty + 1, NCW);
+  }
+  __syncthreads();
+  int ktiles = 0;
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) ++ktiles;
+#if EIK_PROF
+  long long pw = 0, pw2 = 0, pt0 = clock64();
+#define TWP_BEGIN long long w0_ = clock64();
+#define TWP_END(v) v += clock64() - w0_;
+#else
+#define TWP_BEGIN
+#define TWP_END(v)
+#endif
+  if (warp == 0) {
+    // ---------------- TMA issuer
+    if (threadIdx.x == 0) {
+      uint32_t pe[2] = {0u, 0u};
+      for (int k = 0; k < ktiles; ++k) {
+        const int t = blockIdx.x + k * gridDim.x;
+        const int64_t c0 = __ldg(S.t_cell0 + t);
+        const uint32_t nT = (uint32_t)__ldg(S.t_nT + t);
+        for (int h = 0; h < 2; ++h) {
+          if (k >= 1) {
+            mbar_wait(t0.cempty + h, pe[h]);
+            pe[h] ^= 1u;
+          }
+          fence_proxy_async_shared();
+          // runs rounded up to 16 bytes (odd last tile): the extra element is
+          // the next chunk's first (or the allocation's slack), never read
+          const uint32_t run = (nT * 8u + 15u) & ~15u;
+          const uint32_t bytes = run * HALF_RUNS + (h == 1 ? nT * 32u : 0u);
+          mbar_expect_tx(t0.cfull + h, bytes);
+          if (nT > 0) {
+            for (int q = h * HALF_RUNS; q < (h + 1) * HALF_RUNS; ++q)
+              tma_g2s(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run,
+                      t0.cfull + h);
+            if (h == 1) tma_g2s(t0.neb, S.ne + c0, nT * 32u, t0.cfull + h);
+          }
+        }
+      }
+    }
+  } else if (threadIdx.x < PT) {
+    // ---------------- gatherers: steps 1-2
+    const int lt = threadIdx.x - 32;
+    for (int k = 0; k < ktiles; ++k) {
+      const int t = blockIdx.x + k * gridDim.x;
+      const int b = k & 1;
+      const TwSmem ts = tw_smem(S, b);
+      {
+        TWP_BEGIN
+        if (k >= 2) nb_sync(4 + b, NB);
+        TWP_END(pw)
+      }
+      const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+      const int* map = S.e2map + __ldg(S.t_e2off + t);
+      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+      for (int base = 0; base < nE2; base += 2 * GT) {
+        const int ca = base + lt, cb = ca + GT;
+        const bool va = ca < nE2, vb = cb < nE2;
+        const int ga = va ? __ldg(map + ca) : 0;
+        const int gb = vb ? __ldg(map + cb) : 0;
+        double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
+                b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
+        if (va) {
+          a0 = F.src[ga];
+          if (F.vm2) a1 = F.vm2[ga];
+          if (F.vm1) a2 = F.vm1[ga];
+          if (ca < nE1) ua = S.lin[ga];
+        }
+        if (vb) {
+          b0 = F.src[gb];
+          if (F.vm2) b1 = F.vm2[gb];
+          if (F.vm1) b2 = F.vm1[gb];
+          if (cb < nE1) ub = S.lin[gb];
+        }
+        if (va) {
+          const double4 x = form_x(F, a0, a1, a2);
+          sst(ts.x, ca, x);
+          if (ca < nE1) sst(ts.U, ca, ua);
+          if (F.out && ca < nT) F.out[ga] = x;
+        }
+        if (vb) {
+          const double4 x = form_x(F, b0, b1, b2);
+          sst(ts.x, cb, x);
+          if (cb < nE1) sst(ts.U, cb, ub);
+          if (F.out && cb < nT) F.out[gb] = x;
+        }
+      }
+      nb_sync(1, GT);
+      for (int c = lt; c < nE1; c += GT) {
+        const Row8 row = load_row8(rows + (int64_t)c * 8);
+        const double* lc = S.Lc + (int64_t)__ldg(map + c) * 8;
+        const double4 xc = sld(ts.x, c);
+        double4 acc = d4(0.0);
+#pragma unroll
+        for (int s = 0; s < KCMAX; ++s) {
+          const double l = __ldg(lc + s);
+          const double4 xv = sld(ts.x, row.s[s]);
+          acc.x += l * (xv.x - xc.x);
+          acc.y += l * (xv.y - xc.y);
+          acc.z += l * (xv.z - xc.z);
+          acc.w += l * (xv.w - xc.w);
+        }
+        sst(ts.La, c, acc);
+      }
+      nb_arrive(2 + b, NB);
+    }
+    for (int k = ktiles > 2 ? ktiles - 2 : 0; k < ktiles; ++k) nb_sync(4 + (k & 1), NB);
+  } else {
+    // ---------------- consumers: step 3 from shared memory
+    // WS_TPC == 1: one thread per cell, the two coefficient halves in turn
+    //   (half 0 is released to the TMA warp before half 1 is computed);
+    // WS_TPC == 2: adjacent lanes take slots 0-2 / 3-5 of one cell.
+    const int ct = threadIdx.x - PT;
+    const int c = ct / WS_TPC;
+    const int half = ct % WS_TPC;
+    const int lane = threadIdx.x & 31;
+    uint32_t pf[2] = {0u, 0u};
+    for (int k = 0; k < ktiles; ++k) {
+      const int t = blockIdx.x + k * gridDim.x;
+      const int b = k & 1;
+      const TwSmem ts = tw_smem(S, b);
+      const int64_t c0 = __ldg(S.t_cell0 + t);
+      const int nT = __ldg(S.t_nT + t);
+      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+      const bool live = c < nT;
+      const int cc = live ? c : 0;
+      const int64_t i = c0 + cc;
+      // global reads that do not depend on the staged data first
+      const Row8 row = load_row8(rows + (int64_t)cc * 8);
+      double lcr[8];
+      const double* lc = S.Lc + i * 8;
+#pragma unroll
+      for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
+      const double4 vm = (F.epi_vm1 && half == 0) ? F.epi_vm1[i] : d4(0.0);
+      {
+        TWP_BEGIN
+        nb_sync(2 + b, NB);
+        TWP_END(pw)
+      }
+      const double4 ai = sld(ts.x, cc);
+      const double4 Ui = sld(ts.U, cc);
+      const double4 lai = sld(ts.La, cc);
+      JvAcc a;
+      double4 q;
+      if constexpr (WS_TPC == 1) {
+        {
+          TWP_BEGIN
+          mbar_wait(t0.cfull, pf[0]);
+          TWP_END(pw2)
+        }
+        pf[0] ^= 1u;
+        a = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, 0, cc, i, ai, Ui, lai);
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(t0.cempty);
+        {
+          TWP_BEGIN
+          mbar_wait(t0.cfull + 1, pf[1]);
+          TWP_END(pw2)
+        }
+        pf[1] ^= 1u;
+        const JvAcc a2 = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, KCMAX / 2,
+                                                    cc, i, ai, Ui, lai);
+        q = t0.neb[cc];
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(t0.cempty + 1);
+        a.zeta += a2.zeta; a.gx += a2.gx; a.gy += a2.gy; a.gz += a2.gz; a.dv += a2.dv;
+        a.l0 += a2.l0; a.l1 += a2.l1; a.l2 += a2.l2; a.l3 += a2.l3;
+      } else {
+        {
+          TWP_BEGIN
+          mbar_wait(t0.cfull, pf[0]);
+          mbar_wait(t0.cfull + 1, pf[1]);
+          TWP_END(pw2)
+        }
+        pf[0] ^= 1u;
+        pf[1] ^= 1u;
+        a = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, half * (KCMAX / 2), cc,
+                                       i, ai, Ui, lai);
+        q = t0.neb[cc];
+        a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
+        a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
+        a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
+        a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
+        a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
+        a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
+        a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
+        a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
+        a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive1(t0.cempty);
+          mbar_arrive1(t0.cempty + 1);
+        }
+      }
+      if (live && half == 0) {
+        const double4 z = S.scale * swe_jv_finish(S, a, q, ai, Ui);
+        epi(i, z, ai, vm);
+      }
+      nb_arrive(4 + b, NB);
+    }
+  }
+  __syncthreads();
+#if EIK_PROF
+  if (S.prof && (threadIdx.x == 32 || threadIdx.x == PT)) {
+    const int o = threadIdx.x == 32 ? 0 : 2;
+    atomicAdd(S.prof + o, (unsigned long long)pw);
+    atomicAdd(S.prof + o + 1, (unsigned long long)(clock64() - pt0));
+    if (o == 2) atomicAdd(S.prof + 4, (unsigned long long)pw2);
+  }
+#endif
+#undef TWP_BEGIN
+#undef TWP_END
+}
+
 template <class Epi>
 __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
-  if constexpr (WS) {
+  if constexpr (WS == 2) {
+    swe_tiled_tw(sm, S, F, epi);
+    return;
+  } else if constexpr (WS == 1) {
     swe_tiled_ws(sm, S, F, epi);
     return;
   }

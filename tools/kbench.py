@@ -9,7 +9,7 @@ m = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 ops, u0, spec = make_config(name)
 ctx = gswe.SweContext(ops)
-info = (C.c_int64 * 13)()
+info = (C.c_int64 * 14)()
 nat.check(nat.load().eik_swe_info(ctx.h, info))
 print("info G,TPB,tiles,e1max,e2max,K,KC,tiled_ok,smem =", list(info))
 v = np.random.default_rng(0).standard_normal(u0.shape[0])
@@ -24,8 +24,8 @@ print(f"{name} N={N} m={m} reps={reps}: {out[0]:.3f} ms total, {us:.1f} us/iter,
       f"B_alg {balg/1e6:.1f} MB -> {balg/us/1e3:.0f} GB/s ({balg/us/1e3/6543.4*100:.1f}% of 6543.4)")
 nat.check(nat.load().eik_swe_info(ctx.h, info))
 if info[10] and info[12] and len(sys.argv) > 4 and sys.argv[4] == "ws":
-    print("WS: producer wait %.1f%% of its time, consumer wait %.1f%% of its time" % (
-        100 * info[9] / info[10], 100 * info[11] / info[12]))
+    print("WS: producer wait %.1f%% of its time, consumer wait %.1f%% of its time (+ TMA wait %.1f%%)" % (
+        100 * info[9] / info[10], 100 * info[11] / info[12], 100 * info[13] / info[12]))
 elif info[12]:
     tot = info[9] + info[10] + info[11]
     print("tile step cycles share: step1 %.1f%% step2 %.1f%% step3 %.1f%%, per-CTA-call avg %.0f us" % (
