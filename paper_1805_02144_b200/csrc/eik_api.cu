@@ -947,6 +947,49 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
       e2max = std::max(e2max, nE2);
     }
   }
+  // ---- balance: tile t is processed by CTA t % Gt in the kernels; permute
+  // the tiles so that this static assignment is a longest-processing-time
+  // schedule of the per-tile cost (own cells + halo gathers), padding every
+  // CTA to the same count with empty tiles
+  int NTb = NT;
+  {
+    std::vector<double> cost(NT);
+    for (int t = 0; t < NT; ++t) cost[t] = t_nT[t] + 0.6 * t_nE2[t] + 0.3 * t_nE1[t];
+    std::vector<int> order(NT);
+    for (int t = 0; t < NT; ++t) order[t] = t;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::vector<double> load(Gt, 0.0);
+    std::vector<std::vector<int>> lists(Gt);
+    for (int t : order) {
+      int best = 0;
+      for (int g2 = 1; g2 < Gt; ++g2)
+        if (load[g2] < load[best]) best = g2;
+      load[best] += cost[t];
+      lists[best].push_back(t);
+    }
+    size_t per_cta = 0;
+    for (auto& l : lists) per_cta = std::max(per_cta, l.size());
+    NTb = (int)(per_cta * Gt);
+    std::vector<int32_t> c0b(NTb, 0), nTb(NTb, 0), nE1b(NTb, 0), nE2b(NTb, 0), e2b(NTb, 0),
+        e1b(NTb, 0);
+    for (int g2 = 0; g2 < Gt; ++g2)
+      for (size_t k2 = 0; k2 < lists[g2].size(); ++k2) {
+        const int src = lists[g2][k2];
+        const int dst = (int)(k2 * Gt + g2);
+        c0b[dst] = t_cell0[src];
+        nTb[dst] = t_nT[src];
+        nE1b[dst] = t_nE1[src];
+        nE2b[dst] = t_nE2[src];
+        e2b[dst] = t_e2off[src];
+        e1b[dst] = t_e1off[src];
+      }
+    t_cell0.swap(c0b);
+    t_nT.swap(nTb);
+    t_nE1.swap(nE1b);
+    t_nE2.swap(nE2b);
+    t_e2off.swap(e2b);
+    t_e1off.swap(e1b);
+  }
   EikSwe* c = new EikSwe();
   c->N = N;
   c->K = K;
@@ -983,24 +1026,24 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   int *d_tc0, *d_tnT, *d_tnE1, *d_tnE2, *d_te2, *d_te1, *d_e2map;
   short* d_lnbr;
   double* d_Lc;
-  CKC(B.get(&d_tc0, NT));
-  CKC(B.get(&d_tnT, NT));
-  CKC(B.get(&d_tnE1, NT));
-  CKC(B.get(&d_tnE2, NT));
-  CKC(B.get(&d_te2, NT));
-  CKC(B.get(&d_te1, NT));
+  CKC(B.get(&d_tc0, NTb));
+  CKC(B.get(&d_tnT, NTb));
+  CKC(B.get(&d_tnE1, NTb));
+  CKC(B.get(&d_tnE2, NTb));
+  CKC(B.get(&d_te2, NTb));
+  CKC(B.get(&d_te1, NTb));
   CKC(B.get(&d_e2map, e2map.size()));
   CKC(B.get(&d_lnbr, lnbr.size()));
   CKC(B.get(&d_Lc, Lc.size()));
   double* d_coefc;
   CKC(B.get(&d_coefc, coefc.size()));
   CKC(cudaMemcpy(d_coefc, coefc.data(), coefc.size() * 8, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_tc0, t_cell0.data(), NT * 4, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_tnT, t_nT.data(), NT * 4, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_tnE1, t_nE1.data(), NT * 4, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_tnE2, t_nE2.data(), NT * 4, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_te2, t_e2off.data(), NT * 4, cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(d_te1, t_e1off.data(), NT * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tc0, t_cell0.data(), NTb * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnT, t_nT.data(), NTb * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnE1, t_nE1.data(), NTb * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_tnE2, t_nE2.data(), NTb * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_te2, t_e2off.data(), NTb * 4, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(d_te1, t_e1off.data(), NTb * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_e2map, e2map.data(), e2map.size() * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_lnbr, lnbr.data(), lnbr.size() * 2, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_Lc, Lc.data(), Lc.size() * 8, cudaMemcpyHostToDevice));
@@ -1045,7 +1088,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.df1 = d_df1;
   S.dfx = d_dfx;
   S.cnt = d_cnt;
-  S.ntiles = NT;
+  S.ntiles = NTb;
   S.t_cell0 = d_tc0;
   S.t_nT = d_tnT;
   S.t_nE1 = d_tnE1;

@@ -104,3 +104,24 @@ def test_c0_long_run_matches_oracle_live():
                                         spec.steps * spec.dt, tol=spec.tol)
     assert [(r.matvecs, r.substeps) for r in recs[1:]] == steps
     assert rel(recs[-1].u, ref) <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dt", [900.0, 3600.0, 7200.0])
+def test_c1_dt_sweep_matches_oracle(dt):
+    """C1's dt sweep (pEXPRB4): two steps per dt, full state and per-call
+    counters against the oracle port run live (L6)."""
+    ops, u0, _ = make_config("C1")
+    u, calls, per_step = run_gpu(ops, u0, "pexprb43", dt, 2, 1e-8)
+    ref, steps, _, log = integrate_oracle(swe_problem(ops), "pexprb43", u0, dt, 2 * dt,
+                                          tol=1e-8)
+    assert per_step == steps
+    assert calls == [(c[1], c[2], c[3], c[4]) for c in log.calls]
+    assert rel(u, ref) <= TOL
+
+
+@pytest.mark.slow
+def test_c4_l9_exprb42_first_step_matches_reference_golden():
+    """C4 at L9 (2.6M cells): the cold-start EXPRB4 step (rejections and the
+    m jump) against the reference run on the CPU (207 s there)."""
+    _prefix("C4", "c4_exprb42_1", "exprb42", 900.0, 1)
