@@ -19,6 +19,9 @@ using namespace eik;
 
 // ====================================================================== errors
 static thread_local std::string g_err;
+#ifndef EIK_LPT
+#define EIK_LPT 0
+#endif
 // dynamic smem floor: the dense phase keeps its 6 matrices in shared memory
 // for n = m + p + 1 <= 46
 static constexpr size_t kDenseSmemBytes = 128 + (size_t)6 * 46 * 46 * 8;
@@ -951,8 +954,11 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   // the tiles so that this static assignment is a longest-processing-time
   // schedule of the per-tile cost (own cells + halo gathers), padding every
   // CTA to the same count with empty tiles
+  // (measured: LPT scatters the tiles processed concurrently and loses the L2
+  // locality of the halo gathers -- 182 vs 143 us per Krylov iteration at L8 --
+  // so it is off; round-robin keeps every wave a contiguous Hilbert region)
   int NTb = NT;
-  {
+  if (EIK_LPT) {
     std::vector<double> cost(NT);
     for (int t = 0; t < NT; ++t) cost[t] = t_nT[t] + 0.6 * t_nE2[t] + 0.3 * t_nE1[t];
     std::vector<int> order(NT);
