@@ -41,8 +41,6 @@ static eik_status fail(eik_status s, const std::string& msg) {
 __device__ __forceinline__ void smem_init(Smem& sm) {
   if (threadIdx.x == 0) {
     sm.par = 0;
-    sm.bar_init = 0;
-    sm.tphase = 0;
   }
   __syncthreads();
 }
@@ -908,7 +906,6 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   const int NT = (int)(Gt * per);
   int64_t tsz = (N + NT - 1) / NT;
   if (tsz & 1) ++tsz;  // even tiles keep the TMA runs 16-byte aligned
-  const int tma_ok = (EIK_TMA && tiled_ok && (N % 2 == 0)) ? 1 : 0;
   std::vector<int32_t> t_cell0(NT), t_nT(NT), t_nE1(NT), t_nE2(NT), t_e2off(NT), t_e1off(NT);
   std::vector<int32_t> e2map;
   std::vector<int16_t> lnbr;
@@ -1001,7 +998,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
   eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
-                             kSweKernels, 7, tile_smem_bytes(e1max, e2max, tma_ok), Gt);
+                             kSweKernels, 7, tile_smem_bytes(e1max, e2max), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
   int *d_nbr, *d_dfx, *d_cnt;
@@ -1107,7 +1104,6 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.coefc = d_coefc;
   S.KC = KC;
   S.tiled_ok = tiled_ok ? 1 : 0;
-  S.tma = tma_ok;
   S.prof = nullptr;
   if (EIK_PROF) {
     unsigned long long* pr;

@@ -26,10 +26,10 @@ namespace cg = cooperative_groups;
 namespace eik {
 
 #ifndef EIK_TPB
-#define EIK_TPB 512
+#define EIK_TPB 256
 #endif
 #ifndef EIK_MINB
-#define EIK_MINB 1
+#define EIK_MINB 2
 #endif
 constexpr int TPB = EIK_TPB;    // threads per CTA
 constexpr int MINB = EIK_MINB;  // co-resident CTAs per SM (register budget)
@@ -103,8 +103,6 @@ struct Smem {
   double phi[MAXDIM + 4];
   int ival[4];
   int par;      // partial-buffer parity (double buffering, see grid_reduce)
-  int bar_init; // tile mbarrier initialised
-  int tphase;   // tile mbarrier phase
 };
 
 __device__ __forceinline__ void brange(int64_t NU, int64_t& lo, int64_t& hi) {
@@ -218,7 +216,6 @@ struct SweOp {
   const double* Lc;      // [N][8] off-diagonal Laplacian row (cell-major)
   int KC;                // off-diagonal slots
   int tiled_ok;          // compact stencil valid for this operator set
-  int tma;               // stage own-cell coefficients with TMA bulk copies
   unsigned long long* prof;  // EIK_PROF builds: per-step cycle counters
   int e1max, e2max;
 
@@ -341,24 +338,14 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
 // the row's off-diagonal entries -- true for the sphere grid and for the
 // reference's planar operators -- only the off-diagonal slots are stored and
 //   (G e)_i = sum_j G_ij (e_j - e_i),  (D f)_i = sum_j D_ij (f_j + f_i).
-// Dynamic shared memory of one CTA: the tile's vector on E2, its Laplacian
-// and the linearisation state on E1, the E2 local->global map.
-#ifndef EIK_TMA
-#define EIK_TMA 0
-#endif
-#ifndef EIK_L2PF
-#define EIK_L2PF 0
-#endif
-// threads per own cell in the J v step (2: each thread does half the slots)
-#ifndef EIK_TPC
-#define EIK_TPC (EIK_TMA == 2 ? 2 : 1)
-#endif
-constexpr int TPC = EIK_TPC;
-// EIK_WS: warp-specialised tiled pass -- the first half of the CTA gathers
-// and stages tile k+1 (steps 1-2) while the second half computes J x on
-// tile k (step 3); two shared-memory tile buffers, named barriers.
+//
+// Default: the single-role pass at the end of this section (256-thread
+// CTAs, 2 per SM, every thread gathers then computes).  EIK_WS=2 with
+// EIK_TPB=512 selects the TMA warp-specialised pipeline `swe_tiled_tw` (warp
+// 0 bulk-copies coefficients, warps 1-7 gather, warps 8-15 compute); it
+// measured 141 us per Krylov iteration at L8 against 126 us for the default.
 #ifndef EIK_WS
-#define EIK_WS ((EIK_TPB == 512 && EIK_TMA == 0) ? 2 : 0)
+#define EIK_WS 0
 #endif
 constexpr int WS = EIK_WS;
 #ifndef EIK_PT
@@ -367,14 +354,14 @@ constexpr int WS = EIK_WS;
 #ifndef EIK_WS_TPC
 #define EIK_WS_TPC 1
 #endif
-constexpr int PT = EIK_PT;                       // producer threads (WS)
-constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell (WS)
-constexpr int TILE = WS ? (TPB - PT) / WS_TPC : TPB / TPC;  // max own cells per tile
+constexpr int PT = EIK_PT;                       // producer threads (TMA warp + gatherers)
+constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell
+constexpr int TILE = WS ? (TPB - PT) / WS_TPC : TPB;  // max own cells per tile
 static_assert(WS != 2 || TILE == 256, "TMA-WS: 256-cell tiles");
 #ifndef EIK_PROF
 #define EIK_PROF 0
 #endif
-constexpr int NCOEF = KCMAX * 9;  // staged coefficient chunks (slot-major G/D/V)
+constexpr int NCOEF = KCMAX * 9;  // staged coefficient runs (slot-major G/D/V)
 
 #ifndef EIK_SPLIT
 #define EIK_SPLIT 1
@@ -404,44 +391,23 @@ __device__ __forceinline__ void sst(const SArr& a, int l, double4 v) {
 }
 
 struct TileSmem {
-  unsigned long long* bar;  // [2] mbarriers: A = small own-cell blocks, B = coefficients
-  double* cb;               // [NCOEF][TILE] own-cell coefficients (TMA)
-  double4* neb;             // [TILE] own-cell (n, eta) (TMA)
-  double4* vmb;             // [TILE] own-cell v_{j-1} (TMA, EIK_TMA == 2)
-  short* rowb;              // [TILE][8] own-cell local neighbour rows (TMA == 2)
-  double* lcb;              // [TILE][8] own-cell Laplacian rows (TMA == 2)
+  double* cb;  // [NCOEF][TILE] staged own-cell coefficients (TMA pipeline) or null
   SArr x;
   SArr La;
   SArr U;
   int* gid;
 };
 
-__host__ __device__ constexpr size_t tile_tma_bytes(int tma) {
-  return tma == 0 ? 0
-                  : (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
-                        (tma == 2 ? (size_t)TILE * (32 + 16 + 64) : 0);
-}
-
 __host__ __device__ constexpr size_t tile_buf_bytes(int e1max, int e2max) {
   return (size_t)e2max * 32 + (size_t)e1max * 64 + (size_t)e2max * 4 + 16;
 }
 
-__device__ __forceinline__ TileSmem tile_smem(const SweOp& S, int buf = 0) {
+// single-role pass: one tile buffer after a 128-byte header
+__device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TileSmem t;
-  t.bar = reinterpret_cast<unsigned long long*>(dsm);
-  unsigned char* p = dsm + 128 + (size_t)buf * ((tile_buf_bytes(S.e1max, S.e2max) + 127) / 128 * 128);
-  t.cb = reinterpret_cast<double*>(p);
-  unsigned char* p2 = p + (size_t)NCOEF * TILE * 8;
-  t.neb = reinterpret_cast<double4*>(p2);
-  p2 += (size_t)TILE * 32;
-  t.vmb = reinterpret_cast<double4*>(p2);
-  p2 += (size_t)TILE * 32;
-  t.lcb = reinterpret_cast<double*>(p2);
-  p2 += (size_t)TILE * 64;
-  t.rowb = reinterpret_cast<short*>(p2);
-  p += tile_tma_bytes(S.tma);
-  double2* q = reinterpret_cast<double2*>(p);
+  t.cb = nullptr;
+  double2* q = reinterpret_cast<double2*>(dsm + 128);
   t.x = SArr{q, S.e2max};
   q += 2 * S.e2max;
   t.La = SArr{q, S.e1max};
@@ -455,12 +421,10 @@ __device__ __forceinline__ TileSmem tile_smem(const SweOp& S, int buf = 0) {
 __host__ __device__ constexpr size_t tw_buf_bytes(int e1max, int e2max) {
   return ((size_t)e2max * 32 + (size_t)e1max * 64 + 127) / 128 * 128;
 }
-__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max, int tma) {
-  if (WS == 2)
-    return 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 + 2 * tw_buf_bytes(e1max, e2max);
-  return 128 + tile_tma_bytes(tma) +
-         (WS ? 2 * ((tile_buf_bytes(e1max, e2max) + 127) / 128 * 128)
-             : tile_buf_bytes(e1max, e2max));
+__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
+  return WS == 2 ? 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
+                       2 * tw_buf_bytes(e1max, e2max)
+                 : 128 + tile_buf_bytes(e1max, e2max);
 }
 
 // ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
@@ -484,6 +448,22 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t byt
       "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
+// Same copy with an L2 evict-first policy: the coefficient stream (≈ 60 % of
+// the bytes of a Krylov iteration, read once per iteration) must not push
+// the Krylov vectors written by the previous iteration out of the 126 MB L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_g2s_ef(void* dst, const void* src, uint32_t bytes,
+                                           unsigned long long* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -493,13 +473,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase)
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-// Bulk L2 prefetch (sm_90+): pull a contiguous run into L2 without touching
-// registers or shared memory.
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-  if (bytes >= 16)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u)
-                 : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -624,179 +597,12 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
 // the own cells -> epi(i, z, x_i).  A whole Krylov iteration (orthogonalise
 // + normalise v_j, L v_j, J v_j, projections) is one such pass: one HBM
 // sweep and one grid barrier per iteration.
-// Prefetch tile t's own-cell streams into L2 (the own cells are one
-// contiguous Hilbert range): the 54 compact-coefficient runs, the Laplacian
-// rows, (n, eta) and the vectors the pass reads.  Issued by warp 0 one tile
-// ahead so the DRAM stream keeps flowing while the current tile gathers.
-__device__ __forceinline__ void prefetch_tile(const SweOp& S, const Form& F, int t) {
-  if (t >= S.ntiles || threadIdx.x >= 32) return;
-  const int64_t c0 = __ldg(S.t_cell0 + t);
-  const int nT = __ldg(S.t_nT + t);
-  if (nT == 0) return;
-  const uint32_t run = (uint32_t)nT * 8;
-  for (int q = threadIdx.x; q < NCOEF + 7; q += 32) {
-    if (q < NCOEF) l2_prefetch(S.coefc + (int64_t)q * S.N + c0, run);
-    else if (q == NCOEF) l2_prefetch(S.Lc + c0 * 8, (uint32_t)nT * 64);
-    else if (q == NCOEF + 1) l2_prefetch(S.ne + c0, (uint32_t)nT * 32);
-    else if (q == NCOEF + 2) l2_prefetch(F.src + c0, (uint32_t)nT * 32);
-    else if (q == NCOEF + 3 && F.vm1) l2_prefetch(F.vm1 + c0, (uint32_t)nT * 32);
-    else if (q == NCOEF + 4 && F.vm2) l2_prefetch(F.vm2 + c0, (uint32_t)nT * 32);
-    else if (q == NCOEF + 5) l2_prefetch(S.lin + c0, (uint32_t)nT * 32);
-    else if (q == NCOEF + 6) l2_prefetch(S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8,
-                                         (uint32_t)__ldg(S.t_nE1 + t) * 16);
-  }
-}
-
-
-// ---- warp-specialised pipeline (EIK_WS) --------------------------------
 __device__ __forceinline__ void nb_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void nb_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// named barrier ids: 1 producer-internal, 2+b FULL[b], 4+b EMPTY[b]
-template <class Epi>
-__device__ void swe_tiled_ws(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
-  constexpr int HALF = PT;  // producer threads
-  const bool prod = threadIdx.x < HALF;
-  const int lt = prod ? threadIdx.x : threadIdx.x - HALF;
-  int ktiles = 0;
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) ++ktiles;
-#if EIK_PROF
-  long long wt = 0, t0p = clock64();
-#endif
-  if (prod) {
-    for (int k = 0; k < ktiles; ++k) {
-      const int t = blockIdx.x + k * gridDim.x;
-      const int b = k & 1;
-      const TileSmem ts = tile_smem(S, b);
-#if EIK_PROF
-      long long w0 = clock64();
-#endif
-      if (k >= 2) nb_sync(4 + b, TPB);  // consumer released buffer b
-#if EIK_PROF
-      wt += clock64() - w0;
-#endif
-      const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-      const int* map = S.e2map + __ldg(S.t_e2off + t);
-      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-      for (int base = 0; base < nE2; base += 2 * HALF) {
-        const int ca = base + lt, cb = ca + HALF;
-        const bool va = ca < nE2, vb = cb < nE2;
-        const int ga = va ? __ldg(map + ca) : 0;
-        const int gb = vb ? __ldg(map + cb) : 0;
-        double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
-                b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
-        if (va) {
-          a0 = F.src[ga];
-          if (F.vm2) a1 = F.vm2[ga];
-          if (F.vm1) a2 = F.vm1[ga];
-          if (ca < nE1) ua = S.lin[ga];
-        }
-        if (vb) {
-          b0 = F.src[gb];
-          if (F.vm2) b1 = F.vm2[gb];
-          if (F.vm1) b2 = F.vm1[gb];
-          if (cb < nE1) ub = S.lin[gb];
-        }
-        if (va) {
-          const double4 x = form_x(F, a0, a1, a2);
-          ts.gid[ca] = ga;
-          sst(ts.x, ca, x);
-          if (ca < nE1) sst(ts.U, ca, ua);
-          if (F.out && ca < nT) F.out[ga] = x;
-        }
-        if (vb) {
-          const double4 x = form_x(F, b0, b1, b2);
-          ts.gid[cb] = gb;
-          sst(ts.x, cb, x);
-          if (cb < nE1) sst(ts.U, cb, ub);
-          if (F.out && cb < nT) F.out[gb] = x;
-        }
-      }
-      nb_sync(1, HALF);
-      for (int c = lt; c < nE1; c += HALF) {
-        const Row8 row = load_row8(rows + (int64_t)c * 8);
-        const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
-        const double4 xc = sld(ts.x, c);
-        double4 acc = d4(0.0);
-#pragma unroll
-        for (int s = 0; s < KCMAX; ++s) {
-          const double l = __ldg(lc + s);
-          const double4 xv = sld(ts.x, row.s[s]);
-          acc.x += l * (xv.x - xc.x);
-          acc.y += l * (xv.y - xc.y);
-          acc.z += l * (xv.z - xc.z);
-          acc.w += l * (xv.w - xc.w);
-        }
-        sst(ts.La, c, acc);
-      }
-      nb_arrive(2 + b, TPB);  // buffer b full
-    }
-    // drain the consumer's last releases so the barriers start clean next time
-    for (int k = ktiles > 2 ? ktiles - 2 : 0; k < ktiles; ++k) nb_sync(4 + (k & 1), TPB);
-  } else {
-    for (int k = 0; k < ktiles; ++k) {
-      const int t = blockIdx.x + k * gridDim.x;
-      const int b = k & 1;
-      const TileSmem ts = tile_smem(S, b);
-#if EIK_PROF
-      long long w0 = clock64();
-#endif
-      nb_sync(2 + b, TPB);  // wait for buffer b
-#if EIK_PROF
-      wt += clock64() - w0;
-#endif
-      const int64_t c0 = __ldg(S.t_cell0 + t);
-      const int nT = __ldg(S.t_nT + t);
-      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-      {
-        const int c0l = lt / WS_TPC, part = lt % WS_TPC;
-        const bool live = c0l < nT;
-        const int c = live ? c0l : 0;
-        const int64_t i = c0 + c;
-        const double4 ai = sld(ts.x, c);
-        const double4 Ui = sld(ts.U, c);
-        const double4 lai = sld(ts.La, c);
-        const Row8 row = load_row8(rows + (int64_t)c * 8);
-        const double* lc = S.Lc + i * 8;
-        double lcr[8];
-#pragma unroll
-        for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
-        JvAcc a = swe_jv_part<0, KCMAX / WS_TPC>(S, ts, row.s, lcr, part * (KCMAX / WS_TPC), c,
-                                                  i, ai, Ui, lai);
-        if constexpr (WS_TPC == 2) {
-          a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
-          a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
-          a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
-          a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
-          a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
-          a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
-          a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
-          a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
-          a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
-        }
-        if (live && part == 0) {
-          const double4 z = S.scale * swe_jv_finish(S, a, S.ne[i], ai, Ui);
-          const double4 vm = F.epi_vm1 ? F.epi_vm1[i] : d4(0.0);
-          epi(i, z, ai, vm);
-        }
-      }
-      nb_arrive(4 + b, TPB);  // buffer b free
-    }
-  }
-#if EIK_PROF
-  if (S.prof && (threadIdx.x == 0 || threadIdx.x == PT)) {
-    const int o = threadIdx.x == 0 ? 0 : 2;
-    atomicAdd(S.prof + o, (unsigned long long)wt);                       // wait
-    atomicAdd(S.prof + o + 1, (unsigned long long)(clock64() - t0p));    // total
-  }
-#endif
-  __syncthreads();
-}
-
-
 // ---- TMA warp-specialised pipeline (EIK_WS == 2) ---------------------------
 // warp 0: TMA issuer -- streams each tile's own-cell coefficients (54 runs,
 //         two halves of 3 stencil slots) and (n, eta) into shared memory
@@ -805,8 +611,7 @@ __device__ void swe_tiled_ws(Smem& sm, const SweOp& S, const Form& F, const Epi&
 //         into tile buffer (k+1)&1;
 // warps PT/32..: consumers -- step 3 (J x) from shared memory only.
 struct TwSmem {
-  unsigned long long* cfull;   // [2] coefficient half h landed (tx-count)
-  unsigned long long* cempty;  // [2] consumers released half h (8 warp arrivals)
+  unsigned long long* cfull;   // [NST] stage h landed (tx-count); [NST..2NST) stage released
   double* cb;                  // [NCOEF][TILE]
   double4* neb;                // [TILE]
   SArr x, La, U;               // tile buffer
@@ -815,7 +620,6 @@ __device__ __forceinline__ TwSmem tw_smem(const SweOp& S, int buf) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TwSmem t;
   t.cfull = reinterpret_cast<unsigned long long*>(dsm);
-  t.cempty = t.cfull + 2;
   t.cb = reinterpret_cast<double*>(dsm + 128);
   t.neb = reinterpret_cast<double4*>(dsm + 128 + (size_t)NCOEF * TILE * 8);
   unsigned char* p = dsm + 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
@@ -830,12 +634,7 @@ __device__ __forceinline__ TwSmem tw_smem(const SweOp& S, int buf) {
 }
 __device__ __forceinline__ TileSmem ts_as_tile(const TwSmem& b, const TwSmem& t0) {
   TileSmem r;
-  r.bar = nullptr;
   r.cb = t0.cb;
-  r.neb = t0.neb;
-  r.vmb = nullptr;
-  r.rowb = nullptr;
-  r.lcb = nullptr;
   r.x = b.x;
   r.La = b.La;
   r.U = b.U;
@@ -852,14 +651,19 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
   constexpr int CT = TPB - PT;           // consumer threads (== TILE * WS_TPC)
   constexpr int NB = GT + CT;            // named-barrier participants
   constexpr int NCW = CT / 32;           // consumer warps
-  constexpr int HALF_RUNS = NCOEF / 2;   // 27 runs per half (3 slots x 9 ops)
+#ifndef EIK_NSTAGE
+#define EIK_NSTAGE 3
+#endif
+  constexpr int NST = EIK_NSTAGE;        // coefficient stages (2: halves, 3: thirds)
+  constexpr int SLOTS_PER = KCMAX / NST;
+  constexpr int HALF_RUNS = NCOEF / NST; // runs per stage
   const int warp = threadIdx.x >> 5;
   const TwSmem t0 = tw_smem(S, 0);
   if (threadIdx.x == 0) {
-    mbar_init(t0.cfull, 1);
-    mbar_init(t0.cfull + 1, 1);
-    mbar_init(t0.cempty, NCW);
-    mbar_init(t0.cempty + 1, NCW);
+    for (int h = 0; h < NST; ++h) {
+      mbar_init(t0.cfull + h, 1);
+      mbar_init(t0.cfull + NST + h, NCW);  // cempty
+    }
   }
   __syncthreads();
   int ktiles = 0;
@@ -875,27 +679,29 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
   if (warp == 0) {
     // ---------------- TMA issuer
     if (threadIdx.x == 0) {
-      uint32_t pe[2] = {0u, 0u};
+      uint32_t pe[NST];
+      for (int h = 0; h < NST; ++h) pe[h] = 0u;
+      const uint64_t pol = l2_evict_first_policy();
       for (int k = 0; k < ktiles; ++k) {
         const int t = blockIdx.x + k * gridDim.x;
         const int64_t c0 = __ldg(S.t_cell0 + t);
         const uint32_t nT = (uint32_t)__ldg(S.t_nT + t);
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NST; ++h) {
           if (k >= 1) {
-            mbar_wait(t0.cempty + h, pe[h]);
+            mbar_wait(t0.cfull + NST + h, pe[h]);
             pe[h] ^= 1u;
           }
           fence_proxy_async_shared();
           // runs rounded up to 16 bytes (odd last tile): the extra element is
           // the next chunk's first (or the allocation's slack), never read
           const uint32_t run = (nT * 8u + 15u) & ~15u;
-          const uint32_t bytes = run * HALF_RUNS + (h == 1 ? nT * 32u : 0u);
+          const uint32_t bytes = run * HALF_RUNS + (h == NST - 1 ? nT * 32u : 0u);
           mbar_expect_tx(t0.cfull + h, bytes);
           if (nT > 0) {
             for (int q = h * HALF_RUNS; q < (h + 1) * HALF_RUNS; ++q)
-              tma_g2s(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run,
-                      t0.cfull + h);
-            if (h == 1) tma_g2s(t0.neb, S.ne + c0, nT * 32u, t0.cfull + h);
+              tma_g2s_ef(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run,
+                         t0.cfull + h, pol);
+            if (h == NST - 1) tma_g2s(t0.neb, S.ne + c0, nT * 32u, t0.cfull + h);
           }
         }
       }
@@ -976,7 +782,7 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
     const int c = ct / WS_TPC;
     const int half = ct % WS_TPC;
     const int lane = threadIdx.x & 31;
-    uint32_t pf[2] = {0u, 0u};
+    uint32_t pf[4] = {0u, 0u, 0u, 0u};
     for (int k = 0; k < ktiles; ++k) {
       const int t = blockIdx.x + k * gridDim.x;
       const int b = k & 1;
@@ -994,6 +800,7 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
 #pragma unroll
       for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
       const double4 vm = (F.epi_vm1 && half == 0) ? F.epi_vm1[i] : d4(0.0);
+      // (Lc rows were just read by the gatherers for this tile: L1/L2 hits)
       {
         TWP_BEGIN
         nb_sync(2 + b, NB);
@@ -1005,28 +812,23 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
       JvAcc a;
       double4 q;
       if constexpr (WS_TPC == 1) {
-        {
-          TWP_BEGIN
-          mbar_wait(t0.cfull, pf[0]);
-          TWP_END(pw2)
+        a = JvAcc{0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < NST; ++h) {
+          {
+            TWP_BEGIN
+            mbar_wait(t0.cfull + h, pf[h]);
+            TWP_END(pw2)
+          }
+          pf[h] ^= 1u;
+          const JvAcc a2 = swe_jv_part<1, SLOTS_PER>(S, ts_as_tile(ts, t0), row.s, lcr,
+                                                      h * SLOTS_PER, cc, i, ai, Ui, lai);
+          if (h == NST - 1) q = t0.neb[cc];
+          __syncwarp();
+          if (lane == 0) mbar_arrive1(t0.cfull + NST + h);
+          a.zeta += a2.zeta; a.gx += a2.gx; a.gy += a2.gy; a.gz += a2.gz; a.dv += a2.dv;
+          a.l0 += a2.l0; a.l1 += a2.l1; a.l2 += a2.l2; a.l3 += a2.l3;
         }
-        pf[0] ^= 1u;
-        a = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, 0, cc, i, ai, Ui, lai);
-        __syncwarp();
-        if (lane == 0) mbar_arrive1(t0.cempty);
-        {
-          TWP_BEGIN
-          mbar_wait(t0.cfull + 1, pf[1]);
-          TWP_END(pw2)
-        }
-        pf[1] ^= 1u;
-        const JvAcc a2 = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, KCMAX / 2,
-                                                    cc, i, ai, Ui, lai);
-        q = t0.neb[cc];
-        __syncwarp();
-        if (lane == 0) mbar_arrive1(t0.cempty + 1);
-        a.zeta += a2.zeta; a.gx += a2.gx; a.gy += a2.gy; a.gz += a2.gz; a.dv += a2.dv;
-        a.l0 += a2.l0; a.l1 += a2.l1; a.l2 += a2.l2; a.l3 += a2.l3;
       } else {
         {
           TWP_BEGIN
@@ -1050,8 +852,8 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
         a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive1(t0.cempty);
-          mbar_arrive1(t0.cempty + 1);
+          mbar_arrive1(t0.cfull + NST);
+          mbar_arrive1(t0.cfull + NST + 1);
         }
       }
       if (live && half == 0) {
@@ -1074,90 +876,27 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
 #undef TWP_END
 }
 
+// Single-role tiled pass (the default): every thread does the
+// three steps of a tile in turn, separated by __syncthreads.
 template <class Epi>
 __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
   if constexpr (WS == 2) {
     swe_tiled_tw(sm, S, F, epi);
     return;
-  } else if constexpr (WS == 1) {
-    swe_tiled_ws(sm, S, F, epi);
-    return;
   }
   const TileSmem ts = tile_smem(S);
-  const int tma = S.tma;
-  if (tma && threadIdx.x == 0 && !sm.bar_init) {
-    mbar_init(ts.bar, 1);
-    mbar_init(ts.bar + 1, 1);
-    sm.bar_init = 1;
-  }
-  __syncthreads();
-  uint32_t ph = (uint32_t)sm.tphase;  // per-thread copy of the mbarrier phase
-#if EIK_PROF
-  long long pt0 = clock64(), pt1, pacc[4] = {0, 0, 0, 0};
-#endif
-#if EIK_L2PF
-  prefetch_tile(S, F, blockIdx.x);
-#endif
-  // the first round of step 1 uses local->global indices fetched one tile
-  // ahead (they are loaded while the previous tile's steps 2-3 run)
-  int pga = 0, pgb = 0;
-  if (blockIdx.x < S.ntiles) {
-    const int* m0 = S.e2map + __ldg(S.t_e2off + blockIdx.x);
-    const int n0 = __ldg(S.t_nE2 + blockIdx.x);
-    if ((int)threadIdx.x < n0) pga = __ldg(m0 + threadIdx.x);
-    if ((int)threadIdx.x + TPB < n0) pgb = __ldg(m0 + threadIdx.x + TPB);
-  }
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
-#if EIK_L2PF
-    prefetch_tile(S, F, t + gridDim.x);
-#endif
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-    const int cur_ga = pga, cur_gb = pgb;
-    {
-      const int tn = t + gridDim.x;
-      if (tn < S.ntiles) {
-        const int* mn = S.e2map + __ldg(S.t_e2off + tn);
-        const int nn = __ldg(S.t_nE2 + tn);
-        pga = ((int)threadIdx.x < nn) ? __ldg(mn + threadIdx.x) : 0;
-        pgb = ((int)threadIdx.x + TPB < nn) ? __ldg(mn + threadIdx.x + TPB) : 0;
-      }
-    }
     if (nT == 0) continue;  // uniform over the CTA
     const int* map = S.e2map + __ldg(S.t_e2off + t);
     const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-    if (tma && threadIdx.x < 32) {
-      // stage the tile's own-cell blocks (contiguous runs: own cells are a
-      // contiguous Hilbert range) in shared memory with bulk copies while the
-      // gathers of steps 1-2 are in flight.  A: small blocks, B: coefficients.
-      fence_proxy_async_shared();
-      const uint32_t run = (uint32_t)nT * 8;
-      const bool vmx = (tma == 2) && F.epi_vm1 != nullptr;
-      if (threadIdx.x == 0) {
-        if (tma == 2)
-          mbar_expect_tx(ts.bar, (uint32_t)nT * (32 + 16 + 64) + (vmx ? (uint32_t)nT * 32 : 0u));
-        mbar_expect_tx(ts.bar + 1, run * NCOEF + (tma == 1 ? (uint32_t)nT * 32 : 0u));
-      }
-      __syncwarp();
-      if (tma == 2 && threadIdx.x == 0) {
-        tma_g2s(ts.neb, S.ne + c0, (uint32_t)nT * 32, ts.bar);
-        tma_g2s(ts.rowb, rows, (uint32_t)nT * 16, ts.bar);
-        tma_g2s(ts.lcb, S.Lc + c0 * 8, (uint32_t)nT * 64, ts.bar);
-        if (vmx) tma_g2s(ts.vmb, F.epi_vm1 + c0, (uint32_t)nT * 32, ts.bar);
-      }
-      for (int q = threadIdx.x; q < NCOEF; q += 32)
-        tma_g2s(ts.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run, ts.bar + 1);
-      if (tma == 1 && threadIdx.x == 0) tma_g2s(ts.neb, S.ne + c0, (uint32_t)nT * 32, ts.bar + 1);
-    }
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
-#ifndef EIK_ABL
-#define EIK_ABL 0
-#endif
-    for (int base = 0; base < ((EIK_ABL & 1) ? 0 : nE2); base += 2 * TPB) {
+    for (int base = 0; base < nE2; base += 2 * TPB) {
       const int ca = base + threadIdx.x, cb = ca + TPB;
       const bool va = ca < nE2, vb = cb < nE2;
-      const int ga = !va ? 0 : (base == 0 ? cur_ga : __ldg(map + ca));
-      const int gb = !vb ? 0 : (base == 0 ? cur_gb : __ldg(map + cb));
+      const int ga = va ? __ldg(map + ca) : 0;
+      const int gb = vb ? __ldg(map + cb) : 0;
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
               b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
       if (va) {
@@ -1187,22 +926,16 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
         if (F.out && cb < nT) F.out[gb] = x;
       }
     }
-    if (tma == 2) mbar_wait(ts.bar, ph);
     __syncthreads();
-#if EIK_PROF
-    pt1 = clock64(); pacc[0] += pt1 - pt0; pt0 = pt1;
-#endif
     // step 2: L x on E1 (difference form)
-    for (int c = threadIdx.x; c < ((EIK_ABL & 2) ? 0 : nE1); c += TPB) {
-      const bool own2 = (tma == 2) && c < nT;
-      const Row8 row = own2 ? *reinterpret_cast<const Row8*>(ts.rowb + c * 8)
-                            : load_row8(rows + (int64_t)c * 8);
-      const double* lc = own2 ? ts.lcb + c * 8 : S.Lc + (int64_t)ts.gid[c] * 8;
+    for (int c = threadIdx.x; c < nE1; c += TPB) {
+      const Row8 row = load_row8(rows + (int64_t)c * 8);
+      const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
       const double4 xc = sld(ts.x, c);
       double4 acc = d4(0.0);
 #pragma unroll
       for (int s = 0; s < KCMAX; ++s) {
-        const double l = own2 ? lc[s] : __ldg(lc + s);
+        const double l = __ldg(lc + s);
         const double4 xv = sld(ts.x, row.s[s]);
         acc.x += l * (xv.x - xc.x);
         acc.y += l * (xv.y - xc.y);
@@ -1212,71 +945,24 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       sst(ts.La, c, acc);
     }
     __syncthreads();
-#if EIK_PROF
-    pt1 = clock64(); pacc[1] += pt1 - pt0; pt0 = pt1;
-#endif
-    // step 3: z = scale * J x on the own cells (TPC threads per cell)
-    if (tma) mbar_wait(ts.bar + 1, ph);
-    ph ^= 1u;
-    if (!(EIK_ABL & 4)) {
-      const int c = threadIdx.x / TPC;
-      const int part = threadIdx.x % TPC;
-      const bool live = c < nT;
-      const int cc = live ? c : 0;
-      const int64_t i = c0 + cc;
-      const double4 ai = sld(ts.x, cc);
-      const double4 Ui = sld(ts.U, cc);
-      const double4 lai = sld(ts.La, cc);
-      JvAcc a;
-      if (tma == 2) {
-        a = swe_jv_part<1, KCMAX / TPC>(S, ts, ts.rowb + cc * 8, ts.lcb + cc * 8,
-                                         part * (KCMAX / TPC), cc, i, ai, Ui, lai);
-      } else {
-        const Row8 row = load_row8(rows + (int64_t)cc * 8);
-        const double* lc = S.Lc + i * 8;
-        double lcr[8];
+    // step 3: z = scale * J x on the own cells
+    if ((int)threadIdx.x < nT) {
+      const int c = threadIdx.x;
+      const int64_t i = c0 + c;
+      const double4 ai = sld(ts.x, c);
+      const double4 Ui = sld(ts.U, c);
+      const double4 lai = sld(ts.La, c);
+      const Row8 row = load_row8(rows + (int64_t)c * 8);
+      double lcr[8];
 #pragma unroll
-        for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
-        if (tma == 1)
-          a = swe_jv_part<1, KCMAX / TPC>(S, ts, row.s, lcr, part * (KCMAX / TPC), cc, i, ai,
-                                           Ui, lai);
-        else
-          a = swe_jv_part<0, KCMAX / TPC>(S, ts, row.s, lcr, part * (KCMAX / TPC), cc, i, ai,
-                                           Ui, lai);
-      }
-      if constexpr (TPC == 2) {
-        a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
-        a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
-        a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
-        a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
-        a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
-        a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
-        a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
-        a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
-        a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
-      }
-      if (live && part == 0 && !(EIK_ABL & 4)) {
-        const double4 q = tma ? ts.neb[cc] : S.ne[i];
-        const double4 z = S.scale * swe_jv_finish(S, a, q, ai, Ui);
-        const double4 vm = F.epi_vm1 ? (tma == 2 ? ts.vmb[cc] : F.epi_vm1[i]) : d4(0.0);
-        epi(i, z, ai, vm);
-      }
+      for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(S.Lc + i * 8 + s);
+      const JvAcc a = swe_jv_part<0, KCMAX>(S, ts, row.s, lcr, 0, c, i, ai, Ui, lai);
+      const double4 z = S.scale * swe_jv_finish(S, a, S.ne[i], ai, Ui);
+      const double4 vm = F.epi_vm1 ? F.epi_vm1[i] : d4(0.0);
+      epi(i, z, ai, vm);
     }
     __syncthreads();
-#if EIK_PROF
-    pt1 = clock64(); pacc[2] += pt1 - pt0; pt0 = pt1;
-#endif
   }
-  if (threadIdx.x == 0) sm.tphase = (int)ph;
-  __syncthreads();
-#if EIK_PROF
-  if (threadIdx.x == 0 && S.prof) {
-    atomicAdd(S.prof + 0, (unsigned long long)pacc[0]);
-    atomicAdd(S.prof + 1, (unsigned long long)pacc[1]);
-    atomicAdd(S.prof + 2, (unsigned long long)pacc[2]);
-    atomicAdd(S.prof + 3, 1ull);
-  }
-#endif
 }
 
 struct SrcPtr {

@@ -13,6 +13,8 @@ info = (C.c_int64 * 14)()
 nat.check(nat.load().eik_swe_info(ctx.h, info))
 print("info G,TPB,tiles,e1max,e2max,K,KC,tiled_ok,smem =", list(info))
 v = np.random.default_rng(0).standard_normal(u0.shape[0])
+if "f" in sys.argv[4:]:
+    v = spec.dt * ctx.rhs(u0)
 out = (C.c_double * 2)()
 u = np.ascontiguousarray(u0)
 nat.check(nat.load().eik_swe_krylov_bench(ctx.h, nat.dptr(u), nat.dptr(v), spec.dt, m, reps, out))
