@@ -9,6 +9,7 @@
 #include <map>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,6 +63,17 @@ __global__ void k_cell_to_soa(const double4* __restrict__ d, double* s, int64_t 
   }
 }
 
+// Saved position of a split step between kernels (written by the lead thread
+// of the kernel that hands over, read by every thread of the next one).
+struct alignas(8) StepState {
+  EngineState E;
+  EngineTask T;
+  int64_t nA;
+  const double4* base;
+  const double4* fin;
+  int call, pad;
+};
+
 struct SweArgs {
   SweOp S1;   // J at the linearisation state (scale 1)
   SweOp SD;   // dt * J (the engine operator, integrators.py:117)
@@ -77,6 +89,10 @@ struct SweArgs {
   double* nnz_out;
   double* dbg;         // optional per-row output (nnz per cell)
   EngineTask task;     // engine-level API
+  // split step graph
+  StepState* ss;                    // saved step position (global)
+  cudaGraphConditionalHandle cond;  // loop condition of the graph's while node
+  int resume;                       // 0: first k_swe_cont of the step
 };
 
 // F(w) (+ eta at w when `lin` is w); optional out_v = dt * F.
@@ -222,149 +238,286 @@ __device__ EngineTask base_task(const SweArgs& A) {
   return T;
 }
 
-// ---------------------------------------------------------------- step kernel
-// One whole integrator step (integrators.py:140-224) on the resident state.
-// The engine is invoked from a single call site (a loop over the scheme's
-// 1-3 engine calls) so that one inlined copy of it exists and the operator
-// structs stay in kernel-parameter space (A.S1: J, A.SD: dt*J, lin = u_n).
-__global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
-  __shared__ Smem sm;
-  smem_init(sm);
-  cg::grid_group grid = cg::this_grid();
+// ---------------------------------------------------------------- step kernels
+// One integrator step (integrators.py:140-224) on the resident state
+// (A.S1: J at u_n, A.SD: dt*J, the engine operator).  Per engine call of the
+// scheme: the stage work before it and its task; u_{n+1} = base + fin.
+__device__ __forceinline__ int step_ncalls(int scheme) {
+  return scheme == EIK_EXPRB53 ? 3 : (scheme >= EIK_EXPRB42 ? 2 : 1);
+}
+
+__device__ int step_call_setup(cg::grid_group& grid, Smem& sm, const SweArgs& A, int call,
+                               EngineTask& T, const double4*& base, const double4*& fin) {
   const double dt = A.dt;
   const int scheme = A.scheme;
-  ProfClock pc;
-  int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, dt, true, A.Wk.part);
-  pc.mark(PC_RHS);
-  if (st != EIK_OK) { set_status(A.status, st); return; }
-  const int64_t nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);
-  pc.mark(PC_NNZ);
-  const int ncalls = scheme == EIK_EXPRB53 ? 3 : (scheme >= EIK_EXPRB42 ? 2 : 1);
   const double4* u = A.u;
   double4* Ub = A.Ub;
   double4 *va = A.va, *vb = A.vb, *d2 = A.d2;
   double4* const* W = A.W;
-  const double4* base = u;  // u_{n+1} = base + fin
-  const double4* fin = nullptr;
-  for (int call = 0; call < ncalls && st == EIK_OK; ++call) {
-    // ---- stage work before the engine call; task of this call
-    EngineTask T = base_task(A);
-    T.info_idx = call;
-    T.ns = 1;
-    T.rho[0] = 1.0;
-    const int key = scheme * 4 + call;
-    if (key == EIK_EPI3 * 4) {
-      const double c = (2.0 / 3.0) * dt;
-      st = phase_dev(grid, sm, A.S1, A.uprev, A.fn,
-                     [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
-    } else if (key == EIK_EXPRB42 * 4 + 1) {
-      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
+  int st = EIK_OK;
+  T = base_task(A);
+  T.info_idx = call;
+  T.ns = 1;
+  T.rho[0] = 1.0;
+  const int key = scheme * 4 + call;
+  if (key == EIK_EPI3 * 4) {
+    const double c = (2.0 / 3.0) * dt;
+    st = phase_dev(grid, sm, A.S1, A.uprev, A.fn,
+                   [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
+  } else if (key == EIK_EXPRB42 * 4 + 1) {
+    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
+    grid.sync();
+    const double c = (32.0 / 9.0) * dt;
+    st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                   [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
+  } else if (key == EIK_PEXPRB43 * 4 + 1) {
+    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
+    grid.sync();
+    st = phase_dev(grid, sm, A.S1, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
+                   A.Wk.part);
+    if (st == EIK_OK) {
+      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[1][i]; });  // U3
       grid.sync();
-      const double c = (32.0 / 9.0) * dt;
-      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
-                     [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
-    } else if (key == EIK_PEXPRB43 * 4 + 1) {
-      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
-      grid.sync();
-      st = phase_dev(grid, sm, A.S1, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
-                     A.Wk.part);
-      if (st == EIK_OK) {
-        pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[1][i]; });  // U3
-        grid.sync();
-        st = phase_dev(grid, sm, A.S1, Ub, A.fn,
-                       [&](int64_t i, double4 d3) {
-                         const double4 a = d2[i];
-                         va[i] = dt * ((16.0 * a) - (2.0 * d3));
-                         vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
-                       },
-                       A.Wk.part);
-      }
-    } else if (key == EIK_EXPRB53 * 4 + 1) {
-      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
-      grid.sync();
-      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
-                     [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, A.Wk.part);
-    } else if (key == EIK_EXPRB53 * 4 + 2) {
-      const double c1 = 27.0 / 25.0, c2 = 729.0 / 125.0, q3 = A.c09cube;
-      pointwise(A.S1.N, [&](int64_t i) {
-        const double4 w2 = W[2][i], w3 = W[3][i];
-        const double4 ph = make_double4(w2.x / 0.125, w2.y / 0.125, w2.z / 0.125, w2.w / 0.125);
-        const double4 pn = make_double4(w3.x / q3, w3.y / q3, w3.z / q3, w3.w / q3);
-        Ub[i] = ((u[i] + W[1][i]) + c1 * ph) + c2 * pn;
-      });
-      grid.sync();
-      const double e1 = 250.0 / 81.0, e2 = 500.0 / 27.0;
       st = phase_dev(grid, sm, A.S1, Ub, A.fn,
                      [&](int64_t i, double4 d3) {
                        const double4 a = d2[i];
-                       va[i] = dt * ((18.0 * a) - (e1 * d3));
-                       vb[i] = dt * ((-60.0 * a) + (e2 * d3));
+                       va[i] = dt * ((16.0 * a) - (2.0 * d3));
+                       vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
                      },
                      A.Wk.part);
     }
+  } else if (key == EIK_EXPRB53 * 4 + 1) {
+    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
+    grid.sync();
+    st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                   [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, A.Wk.part);
+  } else if (key == EIK_EXPRB53 * 4 + 2) {
+    const double c1 = 27.0 / 25.0, c2 = 729.0 / 125.0, q3 = A.c09cube;
+    pointwise(A.S1.N, [&](int64_t i) {
+      const double4 w2 = W[2][i], w3 = W[3][i];
+      const double4 ph = make_double4(w2.x / 0.125, w2.y / 0.125, w2.z / 0.125, w2.w / 0.125);
+      const double4 pn = make_double4(w3.x / q3, w3.y / q3, w3.z / q3, w3.w / q3);
+      Ub[i] = ((u[i] + W[1][i]) + c1 * ph) + c2 * pn;
+    });
+    grid.sync();
+    const double e1 = 250.0 / 81.0, e2 = 500.0 / 27.0;
+    st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+                   [&](int64_t i, double4 d3) {
+                     const double4 a = d2[i];
+                     va[i] = dt * ((18.0 * a) - (e1 * d3));
+                     vb[i] = dt * ((-60.0 * a) + (e2 * d3));
+                   },
+                   A.Wk.part);
+  }
+  if (st != EIK_OK) return st;
+  switch (key) {
+    case EIK_RB_EULER * 4:
+      T.p = 1; T.v[1] = A.v1; T.W[0] = W[0]; T.slot = EIK_SLOT_RBE;
+      fin = W[0];
+      break;
+    case EIK_EPI3 * 4:
+      T.p = 2; T.v[1] = A.v1; T.v[2] = va; T.W[0] = W[0]; T.slot = EIK_SLOT_EPI3;
+      fin = W[0];
+      break;
+    case EIK_EXPRB42 * 4:
+      T.p = 1; T.v[1] = A.v1; T.rho[0] = 0.75; T.W[0] = W[0]; T.slot = EIK_SLOT_EXPRB42_1;
+      break;
+    case EIK_EXPRB42 * 4 + 1:
+      T.p = 3; T.v[1] = A.v1; T.v[3] = va; T.W[0] = W[1]; T.slot = EIK_SLOT_EXPRB42_2;
+      fin = W[1];
+      break;
+    case EIK_PEXPRB43 * 4:
+      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 1.0;
+      T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_PEXPRB43_1;
+      break;
+    case EIK_PEXPRB43 * 4 + 1:
+      T.p = 4; T.v[3] = va; T.v[4] = vb; T.W[0] = W[2]; T.slot = EIK_SLOT_PEXPRB43_2;
+      fin = W[2];
+      base = Ub;  // u_{n+1} = U3 + W2
+      break;
+    case EIK_EXPRB53 * 4:
+      T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+      T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_EXPRB53_1;
+      break;
+    case EIK_EXPRB53 * 4 + 1:
+      T.p = 3; T.v[3] = va; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
+      T.W[0] = W[2]; T.W[1] = W[3]; T.slot = EIK_SLOT_EXPRB53_2;
+      break;
+    case EIK_EXPRB53 * 4 + 2:
+      T.p = 4; T.v[1] = A.v1; T.v[3] = va; T.v[4] = vb; T.W[0] = W[4];
+      T.slot = EIK_SLOT_EXPRB53_3;
+      fin = W[4];
+      break;
+    default:
+      return EIK_EINVAL;
+  }
+  return EIK_OK;
+}
+
+// u_prev <- u_n, u_{n+1} = base + fin
+__device__ void step_finish(const SweArgs& A, const double4* base, const double4* fin) {
+  double4* uu = A.u;
+  double4* up = A.uprev;
+  pointwise(A.S1.N, [&](int64_t i) {
+    const double4 old = uu[i];
+    const double4 nb = base[i] + fin[i];
+    up[i] = old;
+    uu[i] = nb;
+  });
+}
+
+// Monolithic step: one cooperative launch with every Krylov sweep inline
+// (used when the split graph below is unavailable, or with EIK_STEP_MONO=1).
+__global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  ProfClock pc;
+  int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, true, A.Wk.part);
+  pc.mark(PC_RHS);
+  if (st != EIK_OK) { set_status(A.status, st); return; }
+  // loop state in local memory: none of it may hold registers across sweeps
+  volatile int64_t nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);
+  pc.mark(PC_NNZ);
+  const double4* volatile base = A.u;
+  const double4* volatile fin = nullptr;
+  __shared__ EngineTask sT;
+  for (volatile int call = 0; call < step_ncalls(A.scheme) && st == EIK_OK; ++call) {
+    EngineTask T;
+    const double4* b = base;
+    const double4* f = fin;
+    st = step_call_setup(grid, sm, A, call, T, b, f);
+    base = b;
+    fin = f;
     pc.mark(PC_DEV);
-    if (st != EIK_OK) break;
-    switch (key) {
-      case EIK_RB_EULER * 4:
-        T.p = 1; T.v[1] = A.v1; T.W[0] = W[0]; T.slot = EIK_SLOT_RBE;
-        fin = W[0];
-        break;
-      case EIK_EPI3 * 4:
-        T.p = 2; T.v[1] = A.v1; T.v[2] = va; T.W[0] = W[0]; T.slot = EIK_SLOT_EPI3;
-        fin = W[0];
-        break;
-      case EIK_EXPRB42 * 4:
-        T.p = 1; T.v[1] = A.v1; T.rho[0] = 0.75; T.W[0] = W[0]; T.slot = EIK_SLOT_EXPRB42_1;
-        break;
-      case EIK_EXPRB42 * 4 + 1:
-        T.p = 3; T.v[1] = A.v1; T.v[3] = va; T.W[0] = W[1]; T.slot = EIK_SLOT_EXPRB42_2;
-        fin = W[1];
-        break;
-      case EIK_PEXPRB43 * 4:
-        T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 1.0;
-        T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_PEXPRB43_1;
-        break;
-      case EIK_PEXPRB43 * 4 + 1:
-        T.p = 4; T.v[3] = va; T.v[4] = vb; T.W[0] = W[2]; T.slot = EIK_SLOT_PEXPRB43_2;
-        fin = W[2];
-        base = Ub;  // u_{n+1} = U3 + W2
-        break;
-      case EIK_EXPRB53 * 4:
-        T.p = 1; T.v[1] = A.v1; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
-        T.W[0] = W[0]; T.W[1] = W[1]; T.slot = EIK_SLOT_EXPRB53_1;
-        break;
-      case EIK_EXPRB53 * 4 + 1:
-        T.p = 3; T.v[3] = va; T.ns = 2; T.rho[0] = 0.5; T.rho[1] = 0.9;
-        T.W[0] = W[2]; T.W[1] = W[3]; T.slot = EIK_SLOT_EXPRB53_2;
-        break;
-      case EIK_EXPRB53 * 4 + 2:
-        T.p = 4; T.v[1] = A.v1; T.v[3] = va; T.v[4] = vb; T.W[0] = W[4];
-        T.slot = EIK_SLOT_EXPRB53_3;
-        fin = W[4];
-        break;
-      default:
-        st = EIK_EINVAL;
-    }
     if (st != EIK_OK) break;
     // the task lives in shared memory during the call: its fields are read a
     // few times per attempt and must not occupy registers across the sweep
-    __shared__ EngineTask sT;
     if (threadIdx.x == 0) sT = T;
     __syncthreads();
     st = engine_call(grid, sm, A.SD, sT, A.Wk, nA);
     pc.skip();
   }
-  if (st == EIK_OK) {
-    double4* uu = A.u;
-    double4* up = A.uprev;
-    pointwise(A.S1.N, [&](int64_t i) {
-      const double4 old = uu[i];
-      const double4 nb = base[i] + fin[i];
-      up[i] = old;
-      uu[i] = nb;
-    });
-  }
+  if (st == EIK_OK) step_finish(A, base, fin);
   set_status(A.status, st);
+}
+
+// Split step (the default): the graph  cont ; while (cond) { sweep ; cont }.
+// k_swe_cont runs the step from its saved position up to the next tiled
+// Krylov sweep, saves the position and sets the loop condition; k_swe_sweep
+// runs that sweep as a kernel of its own, so the sweep is compiled with the
+// whole register budget and no controller state live across it.
+__device__ void cont_stop(const SweArgs& A, int st) {
+  set_status(A.status, st);
+  if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(A.cond, 0u);
+}
+
+__global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (lead) atomicAdd(A.Wk.kiters + 2, 1ull);
+  ProfClock pc;
+  EngineState state;
+  ES& E = state;
+  __shared__ EngineTask sT;
+  volatile int64_t nA;
+  const double4* volatile base;
+  const double4* volatile fin;
+  volatile int call;
+  volatile int in_engine;
+  StepState* G = A.ss;
+  if (!A.resume) {
+    const int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, true, A.Wk.part);
+    pc.mark(PC_RHS);
+    if (st != EIK_OK) { cont_stop(A, st); return; }
+    nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);
+    pc.mark(PC_NNZ);
+    base = A.u;
+    fin = nullptr;
+    call = 0;
+    in_engine = 0;
+  } else {
+    words_load(E, &G->E);
+    if (threadIdx.x == 0) sT = G->T;
+    nA = G->nA;
+    base = G->base;
+    fin = G->fin;
+    call = G->call;
+    in_engine = 1;
+    __syncthreads();
+    pc.skip();
+    if (E.mode == EM_AFTER_SWEEP) eng_finish_attempt(grid, sm, A.SD, sT, A.Wk, E);
+  }
+  for (;;) {
+    if (!in_engine) {
+      if (call >= step_ncalls(A.scheme)) {
+        step_finish(A, base, fin);
+        cont_stop(A, EIK_OK);
+        return;
+      }
+      EngineTask T;
+      const double4* b = base;
+      const double4* f = fin;
+      const int st = step_call_setup(grid, sm, A, call, T, b, f);
+      base = b;
+      fin = f;
+      pc.mark(PC_DEV);
+      if (st != EIK_OK) { cont_stop(A, st); return; }
+      if (threadIdx.x == 0) sT = T;
+      __syncthreads();
+      if (!eng_prologue(grid, sm, sT, A.Wk, nA, E)) {
+        call = call + 1;
+        continue;
+      }
+      in_engine = 1;
+    }
+    const int r = eng_attempt(grid, sm, A.SD, sT, A.Wk, E);
+    if (r == ER_SWEEP) {
+      // every CTA read G at entry and has passed a grid barrier since
+      E.mode = EM_SWEEP;
+      if (lead) {
+        words_store(&G->E, E);
+        G->T = sT;
+        G->nA = nA;
+        G->base = base;
+        G->fin = fin;
+        G->call = call;
+        cudaGraphSetConditional(A.cond, 1u);
+      }
+      return;
+    }
+    if (r == ER_FAIL) { cont_stop(A, EIK_EPHIPM); return; }
+    if (r == ER_DONE) {
+      eng_epilogue(grid, sT, A.Wk, E);
+      call = call + 1;
+      in_engine = 0;
+      continue;
+    }
+    eng_finish_attempt(grid, sm, A.SD, sT, A.Wk, E);
+  }
+}
+
+__global__ void __launch_bounds__(TPB, MINB) k_swe_sweep(SweArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (lead) atomicAdd(A.Wk.kiters + 2, 1ull);
+  ProfClock pc;
+  StepState* G = A.ss;
+  const double4* wp = G->E.wp;
+  const double beta = G->E.beta;
+  const int64_t m_eff = G->E.m_eff;
+  int64_t kmv = 0;
+  const KrylovState ks = krylov_tiled(grid, sm, A.SD, A.Wk, wp, beta, m_eff, kmv);
+  // every CTA read G before the sweep's first grid barrier
+  if (lead) {
+    ES& GE = G->E;
+    eng_store_sweep(GE, ks, kmv);
+  }
+  pc.mark(PC_KRYLOV);
 }
 
 // ------------------------------------------------------- API-level kernels
@@ -711,6 +864,8 @@ struct EikSwe {
   int g_scheme = -1;
   double g_dt = 0.0, g_tol = 0.0;
   bool graphs_ok = true;
+  bool split = getenv("EIK_STEP_MONO") == nullptr;  // split step graph
+  StepState* ss = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.0f;
   double* pinned = nullptr;  // pinned staging for host copies (4N doubles)
@@ -778,7 +933,8 @@ struct EikCsr {
   int64_t nnz = 0;
 };
 
-static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_rhs,
+static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_cont,
+                                    (const void*)k_swe_sweep, (const void*)k_swe_rhs,
                                     (const void*)k_swe_jv, (const void*)k_swe_nnz,
                                     (const void*)k_swe_phipm, (const void*)k_swe_kbench,
                                     (const void*)k_swe_diag};
@@ -998,7 +1154,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
   eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
-                             kSweKernels, 7, tile_smem_bytes(e1max, e2max), Gt);
+                             kSweKernels, 9, tile_smem_bytes(e1max, e2max), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
   int *d_nbr, *d_dfx, *d_cnt;
@@ -1063,6 +1219,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&c->vb, N));
   CKC(B.get(&c->d2, N));
   CKC(B.get(&c->Ub, N));
+  CKC(B.get(&c->ss, 1));
   for (int k = 0; k < 5; ++k) CKC(B.get(&c->W[k], N));
   CKC(B.get(&c->x, N));
   CKC(B.get(&c->out, N));
@@ -1238,32 +1395,80 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
   return EIK_OK;
 }
 
+// The step graph.  Split (default):  k_swe_cont ; while (cond) { k_swe_sweep ;
+// k_swe_cont }  with the loop condition set on the device.  Monolithic
+// (EIK_STEP_MONO=1, or when the conditional graph cannot be built): one
+// k_swe_step launch.
+static bool capture_launches(cudaStream_t st, cudaGraph_t g, const void* const* fns,
+                             SweArgs* args, int nk, int G, size_t smem) {
+  if (cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return false;
+  bool ok = true;
+  for (int k = 0; k < nk && ok; ++k) {
+    void* kargs[] = {&args[k]};
+    ok = cudaLaunchCooperativeKernel(fns[k], G, TPB, kargs, smem, st) == cudaSuccess;
+  }
+  cudaGraph_t out = g;
+  ok = (cudaStreamEndCapture(st, &out) == cudaSuccess) && ok;
+  return ok;
+}
+
+static bool build_step_graph(EikSwe* c, const SweArgs& A, bool split, cudaGraphExec_t* exec) {
+  cudaGraph_t g = nullptr;
+  bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+  if (ok && !split) {
+    SweArgs A0 = A;
+    const void* f0[] = {(const void*)k_swe_step};
+    ok = capture_launches(c->eng.st, g, f0, &A0, 1, c->eng.G, c->eng.smem);
+  } else if (ok) {
+    cudaGraphConditionalHandle h = 0;
+    ok = cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+    SweArgs A0 = A, A1[2] = {A, A};
+    A0.cond = A1[0].cond = A1[1].cond = h;
+    A0.resume = 0;
+    A1[0].resume = A1[1].resume = 1;
+    const void* f0[] = {(const void*)k_swe_cont};
+    const void* f1[] = {(const void*)k_swe_sweep, (const void*)k_swe_cont};
+    ok = ok && capture_launches(c->eng.st, g, f0, &A0, 1, c->eng.G, c->eng.smem);
+    cudaGraphNode_t first = nullptr;
+    size_t nn = 1;
+    ok = ok && cudaGraphGetNodes(g, &first, &nn) == cudaSuccess && nn == 1;
+    alignas(cudaGraphNodeParams) unsigned char cp_raw[sizeof(cudaGraphNodeParams)] = {};
+    cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cp_raw);
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn = nullptr;
+    ok = ok && cudaGraphAddNode(&cn, g, &first, 1, &cp) == cudaSuccess;
+    ok = ok && capture_launches(c->eng.st, cp.conditional.phGraph_out[0], f1, A1, 2, c->eng.G,
+                                c->eng.smem);
+  }
+  ok = ok && cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
+  if (g) cudaGraphDestroy(g);
+  if (!ok) {
+    cudaGetLastError();
+    *exec = nullptr;
+  }
+  return ok;
+}
+
 static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol) {
   SweArgs A = c->args(c->u, dt);
   A.dt = dt;
   A.tol = tol;
   A.scheme = scheme;
+  A.ss = c->ss;
   if (c->graphs_ok) {
     if (!c->gexec || c->g_scheme != scheme || c->g_dt != dt || c->g_tol != tol) {
       if (c->gexec) {
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
       }
-      cudaGraph_t graph = nullptr;
-      bool ok = cudaStreamBeginCapture(c->eng.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-      if (ok) {
-        void* kargs[] = {&A};
-        ok = cudaLaunchCooperativeKernel((const void*)k_swe_step, c->eng.G, TPB, kargs,
-                                         c->eng.smem, c->eng.st) == cudaSuccess;
-        ok = (cudaStreamEndCapture(c->eng.st, &graph) == cudaSuccess) && ok;
-      }
-      if (ok) ok = cudaGraphInstantiate(&c->gexec, graph, 0) == cudaSuccess;
-      if (graph) cudaGraphDestroy(graph);
-      if (!ok) {
-        cudaGetLastError();
-        c->graphs_ok = false;
-        c->gexec = nullptr;
-      } else {
+      if (c->split && !build_step_graph(c, A, true, &c->gexec)) c->split = false;
+      if (!c->split && !build_step_graph(c, A, false, &c->gexec)) c->graphs_ok = false;
+      if (c->gexec) {
         c->g_scheme = scheme;
         c->g_dt = dt;
         c->g_tol = tol;
@@ -1271,7 +1476,7 @@ static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol)
     }
     if (c->graphs_ok) {
       CK(cudaGraphLaunch(c->gexec, c->eng.st));
-      ++c->eng.launches;
+      if (!c->split) ++c->eng.launches;  // split: kernels are counted on the device
       return EIK_OK;
     }
   }
@@ -1438,7 +1643,12 @@ int eik_prof_read(double* out, int reset) {
   return EIK_PROF ? EIK_OK : EIK_EINVAL;
 }
 
-int64_t eik_swe_launches(const EikSwe* c) { return c ? c->eng.launches : 0; }
+int64_t eik_swe_launches(const EikSwe* c) {
+  if (!c) return 0;
+  unsigned long long v[3] = {0, 0, 0};  // [2]: split-step kernels, counted on the device
+  cudaMemcpy(v, c->eng.kiters_d, sizeof(v), cudaMemcpyDeviceToHost);
+  return c->eng.launches + (int64_t)v[2];
+}
 double eik_swe_last_kernel_ms(const EikSwe* c) { return c ? (double)c->last_ms : 0.0; }
 int64_t eik_swe_krylov_iters(const EikSwe* c) {
   if (!c) return 0;

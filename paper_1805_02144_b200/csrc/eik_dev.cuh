@@ -1424,19 +1424,62 @@ __device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp&
   return out;
 }
 
-// phipm_simul_iom2 (phipm.py:291-370); returns an eik_status, uniformly in
-// every CTA.
-template <class Op>
-__device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
-                           const EngineTask& T, const EngineWork& Wk, int64_t nnz) {
+// ---------------------------------------------------------------- engine
+// phipm_simul_iom2 (phipm.py:291-370) as a resumable state machine.  Every
+// thread of every CTA runs the controller redundantly on identical values,
+// so its state needs no broadcast: each thread keeps it in local memory
+// (`EngineState`, accessed through a volatile reference so that none of it
+// holds registers across the Krylov sweep).  The split step (k_swe_cont /
+// k_swe_sweep in eik_api.cu) hands the state from kernel to kernel through
+// global memory, written by the lead thread; the monolithic kernels run the
+// sweep inline.
+enum { EM_ATTEMPT = 0, EM_SWEEP, EM_AFTER_SWEEP };
+enum { ER_DONE = 0, ER_SWEEP, ER_FAIL, ER_CONTINUE };
+
+struct alignas(8) EngineState {
+  // controller (phipm.py:318-359)
+  double t, t_out, tau, tau_nom;
+  int64_t m, m_cap, attempts, acc, rej, mv, nnz;
+  const double4* y;
+  int mode, p, io, y_nz, ycur, hits;
+  unsigned vnzm;  // bit l: v_l is nonzero
+  int wp_nz;
+  // current attempt: Krylov input w_p / beta and the sweep's result
+  const double4* wp;
+  double beta;
+  int64_t m_eff, keep;
+  double hnext, h1, h2;
+  const double4* vz;
+  const double4* vm1;
+  const double4* vv;
+  int broke, expl;
+};
+using ES = volatile EngineState;
+static_assert(sizeof(EngineState) % 8 == 0, "EngineState is copied as 8-byte words");
+
+template <class T>
+__device__ __forceinline__ void words_load(volatile T& dst, const T* src) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(&dst);
+  for (int k = 0; k < (int)(sizeof(T) / 8); ++k) d[k] = __ldcg(s + k);
+}
+template <class T>
+__device__ __forceinline__ void words_store(T* dst, const volatile T& src) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+  const volatile unsigned long long* s = reinterpret_cast<const volatile unsigned long long*>(&src);
+  for (int k = 0; k < (int)(sizeof(T) / 8); ++k) __stcg(d + k, s[k]);
+}
+
+// Exact nonzero flags of v_l (the reference's vl.any()), warm-start seeds and
+// the initial (tau, m) (phipm.py:300-317).  Returns false -- W = 0 written,
+// info marked skipped -- when every v_l is zero (integrators.py:125-127).
+__device__ bool eng_prologue(cg::grid_group& grid, Smem& sm, const EngineTask& T,
+                             const EngineWork& Wk, int64_t nnz, ES& E) {
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  const int64_t NU = Wk.NU, n = Wk.n;
   const int p = T.p;
   int64_t lo, hi;
-  brange(NU, lo, hi);
-
-  // ---- exact nonzero flags of v_l (the reference's vl.any())
-  bool vnz[MAXV];
+  brange(Wk.NU, lo, hi);
+  unsigned mask = 0;
   {
     double c[NPART];
 #pragma unroll
@@ -1447,25 +1490,21 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
         if (l <= p && T.v[l]) c[l] += nz4(T.v[l][u]);
     }
     grid_reduce<NPART>(grid, sm, c, Wk.part);
-    bool any = false;
 #pragma unroll
-    for (int l = 0; l < MAXV; ++l) {
-      vnz[l] = (l <= p) && T.v[l] && c[l] > 0.0;
-      any |= vnz[l];
-    }
-    if (!any) {  // integrators.py:125-127: W = 0, no engine call
-      for (int i = 0; i < T.ns; ++i)
-        for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) T.W[i][u] = d4(0.0);
-      if (lead) {
-        EikPhipmInfo inf = {};
-        inf.skipped = 1;
-        Wk.info[T.info_idx] = inf;
-      }
-      grid.sync();
-      return EIK_OK;
-    }
+    for (int l = 0; l < MAXV; ++l)
+      if ((l <= p) && T.v[l] && c[l] > 0.0) mask |= 1u << l;
   }
-
+  if (!mask) {
+    for (int i = 0; i < T.ns; ++i)
+      for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) T.W[i][u] = d4(0.0);
+    if (lead) {
+      EikPhipmInfo inf = {};
+      inf.skipped = 1;
+      Wk.info[T.info_idx] = inf;
+    }
+    grid.sync();
+    return false;
+  }
   double tau0 = T.tau_init;
   int64_t m0 = T.m_init;
   if (T.slot >= 0) {
@@ -1474,371 +1513,467 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
   }
   double tau_i;
   int64_t m_i;
+  const int64_t n = Wk.n;
   initial_tau_m(tau0, m0, T.rho[0], T.rho[T.ns - 1], T.m_max, n, &tau_i, &m_i);
-  const int64_t m_cap = T.m_max < n ? T.m_max : n;
+  E.mode = EM_ATTEMPT;
+  E.p = p;
+  E.vnzm = mask;
+  E.nnz = nnz;
+  E.m_cap = T.m_max < n ? T.m_max : n;
+  E.tau = tau_i;
+  E.m = m_i;
+  E.y = (mask & 1u) ? T.v[0] : Wk.zero;
+  E.y_nz = (mask & 1u) ? 1 : 0;
+  E.ycur = -1;
+  E.t = 0.0;
+  E.io = 0;
+  E.t_out = T.rho[0];
+  E.attempts = E.acc = E.rej = E.mv = 0;
+  return true;
+}
 
-  // The engine's scalar state is kept in (L1-resident) local memory rather
-  // than registers: it is touched a few times per attempt, while the Krylov
-  // sweep in between needs every register for loads in flight.
-  volatile double tau = tau_i;
-  volatile int64_t m = m_i;
-  const double4* volatile y = vnz[0] ? T.v[0] : Wk.zero;
-  volatile bool y_nz = vnz[0];
-  volatile int ycur = -1;
-  volatile double t = 0.0;
-  volatile int64_t attempts = 0, acc = 0, rej = 0, mv = 0;
-  const int64_t ld = Wk.m_alloc;
+// Next attempt: write finished output points, then the w recurrence
+// (phipm.py:159-182) and the Krylov set-up.  ER_DONE: every output written;
+// ER_FAIL: attempt budget exhausted (info written); ER_SWEEP: the tiled IOM2
+// sweep is due (the caller runs it inline or as its own kernel);
+// ER_CONTINUE: the decomposition is complete here (generic operators, or a
+// zero w_p), dense phase next.
+template <class Op>
+__device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const EngineTask& T,
+                           const EngineWork& Wk, ES& E) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int64_t NU = Wk.NU, n = Wk.n, ld = Wk.m_alloc;
+  int64_t lo, hi;
+  brange(NU, lo, hi);
+  for (;;) {
+    if (E.io >= T.ns) return ER_DONE;
+    if (E.t < E.t_out) break;
+    const double4* y = E.y;
+    double4* Wo = T.W[E.io];
+    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) Wo[u] = y[u];
+    E.io = E.io + 1;
+    if (E.io < T.ns) E.t_out = T.rho[E.io];
+  }
+  E.attempts = E.attempts + 1;
+  if (E.attempts > T.max_attempts) {
+    if (lead) {
+      EikPhipmInfo inf = {};
+      inf.substeps = E.acc;
+      inf.rejections = E.rej;
+      inf.matvecs = E.mv;
+      inf.tau_final = E.tau;
+      inf.m_final = E.m;
+      inf.t_reached = E.t;
+      inf.attempts = E.attempts - 1;
+      inf.status = EIK_EPHIPM;
+      Wk.info[T.info_idx] = inf;
+    }
+    grid.sync();
+    return ER_FAIL;
+  }
+  E.tau_nom = E.tau;
+  {
+    const bool hits = eik_add(E.t, E.tau) >= E.t_out;
+    E.hits = hits ? 1 : 0;
+    if (hits) E.tau = eik_sub(E.t_out, E.t);
+  }
 
-  for (int io = 0; io < T.ns; ++io) {
-    const double t_out = T.rho[io];
-    while (t < t_out) {
-      ++attempts;
-      if (attempts > T.max_attempts) {
-        if (lead) {
-          EikPhipmInfo inf = {};
-          inf.substeps = acc;
-          inf.rejections = rej;
-          inf.matvecs = mv;
-          inf.tau_final = tau;
-          inf.m_final = m;
-          inf.t_reached = t;
-          inf.attempts = attempts - 1;
-          inf.status = EIK_EPHIPM;
-          Wk.info[T.info_idx] = inf;
-        }
-        grid.sync();
-        return EIK_EPHIPM;
-      }
-      const double tau_nom = tau;
-      const bool hits = eik_add(t, tau) >= t_out;
-      if (hits) tau = eik_sub(t_out, t);
-
-      ProfClock pc;
-      // ---- w recurrence (phipm.py:159-182)
-      const double4* wprev = y;
-      bool wprev_nz = y_nz;
-      double ssq = 0.0;
-      for (int j = 1; j <= p; ++j) {
-        double cl[MAXV];
-        for (int ell = 0; ell <= p - j; ++ell) cl[ell] = pow_over_fact(t, ell);
-        const bool do_mv = !(T.zero_skip && !wprev_nz);
-        double4* wj = Wk.w[j];
-        double r[2] = {0.0, 0.0};
-        bool tiled_mv = false;
-        if constexpr (Op::kTiled) tiled_mv = op.tiled_ok && do_mv;
-        if constexpr (Op::kTiled) {
-          if (tiled_mv) {
-            ++mv;
-            Form F{wprev, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
-            swe_tiled(sm, op, F,
-                      [&](int64_t i, double4 z, double4, double4) {
-                        double4 a = z;
-                        for (int ell = 0; ell <= p - j; ++ell)
-                          if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][i];
-                        wj[i] = a;
-                        r[0] += nz4(a);
-                        r[1] += dot4(a, a);
-                      });
-          }
-        }
-        if (!tiled_mv) {
-          if (do_mv) {
-            op_pre(op, wprev, 1.0, lo, hi);
-            grid.sync();
-            ++mv;
-          }
-        }
-        if (!tiled_mv) {
-          for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-            double4 a = do_mv ? op_main(op, wprev, u) : d4(0.0);
-            for (int ell = 0; ell <= p - j; ++ell)
-              if (vnz[j + ell]) a = a + cl[ell] * T.v[j + ell][u];
-            wj[u] = a;
-            r[0] += nz4(a);
-            r[1] += dot4(a, a);
-          }
-        }
-        grid_reduce<2>(grid, sm, r, Wk.part);
-        wprev = wj;
-        wprev_nz = r[0] > 0.0;
-        ssq = r[1];
-      }
-      if (p == 0) {
-        double r[2] = {0.0, 0.0};
-        for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-            const double4 a = y[u];
-            r[0] += nz4(a);
-            r[1] += dot4(a, a);
-          }
-        grid_reduce<2>(grid, sm, r, Wk.part);
-        wprev_nz = r[0] > 0.0;
-        ssq = r[1];
-      }
-      const double4* wp = wprev;
-      const bool wp_nz = wprev_nz;
-      pc.mark(PC_WREC);
-
-      // ---- IOM2 Krylov decomposition (krylov.py:53-112)
-      double beta = 0.0, hnext = 0.0, eps = 0.0, nh = 0.0, corner = 0.0;
-      bool broke = false;
-      int64_t keep = 0;
-      // v_{m+1} = ((z - h1 v_{m-1}) - h2 v_m) / h_next (tiled path) or z / h_next
-      const double4* vnext_z = Wk.zbuf;
-      const double4* vnext_m1 = nullptr;
-      const double4* vnext_v = nullptr;
-      double vnext_h1 = 0.0, vnext_h2 = 0.0;
-      bool vnext_expl = true;
-      if (wp_nz) {
-        beta = sqrt(ssq);
-        const int64_t m_eff = m < n ? m : n;
-        const int64_t iom = m_eff < n ? T.iom : n;
-        if (blockIdx.x == 0) {
-          for (int64_t q = threadIdx.x; q < m_eff * ld; q += TPB) Wk.H[q] = 0.0;
-          __syncthreads();
-        }
-        double hcur = beta;
-        const double4* raw = wp;
-        keep = m_eff;
-        bool tiled_done = false;
-        if constexpr (Op::kTiled) {
-          if (iom == 2 && op.tiled_ok) {
-            tiled_done = true;
-            // one tiled pass + one grid barrier per iteration: v_j is formed
-            // on the fly from (z_{j-1}, v_{j-2}, v_{j-1}) with the previous
-            // iteration's MGS coefficients, its norm taken from the Gram
-            // identity (explicit pass only when that would cancel)
-            int64_t kmv = 0;
-            KrylovState ks = krylov_tiled(grid, sm, op, Wk, wp, beta, m_eff, kmv);
-            mv += kmv;
-            keep = ks.keep;
-            broke = ks.broke;
-            hnext = ks.hnext;
-            vnext_z = ks.vz;
-            vnext_h1 = ks.h1;
-            vnext_h2 = ks.h2;
-            vnext_m1 = ks.vm1;
-            vnext_v = ks.vv;
-            vnext_expl = ks.expl;
-          }
-        }
-        for (int64_t j = 0; j < m_eff && !tiled_done; ++j) {
-          double4* vj = Wk.basis + j * NU;
-          const double4* vjm = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
-          // v_j = raw / h (exact division), La = L v_j
-          for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) vj[u] = div4(raw[u], hcur);
-          op_pre(op, raw, 1.0 / hcur, lo, hi);
-          grid.sync();
-          // z = A v_j + projections
-          double d[3] = {0.0, 0.0, 0.0};
-          const bool fast = (iom == 2);
-          for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-            const double4 z = op_main(op, vj, u);
-            Wk.zbuf[u] = z;
-            if (fast) {
-              const double4 a = vj[u];
-              d[1] += dot4(a, z);
-              if (vjm) {
-                const double4 b = vjm[u];
-                d[0] += dot4(b, z);
-                d[2] += dot4(a, b);
-              }
-            }
-          }
-          ++mv;
-          if (lead) atomicAdd(Wk.kiters, 1ull);
-          double ssz = 0.0;
-          if (fast) {
-            grid_reduce<3>(grid, sm, d, Wk.part);
-            // MGS against v_{j-1} then v_j: <v_j, z - h1 v_{j-1}> = d1 - h1 d2
-            const double h1 = d[0];
-            const double h2 = vjm ? d[1] - h1 * d[2] : d[1];
-            if (lead) {
-              if (vjm) Wk.H[(j - 1) * ld + j] = h1;
-              Wk.H[j * ld + j] = h2;
-            }
-            double r[1] = {0.0};
-            for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-              double4 z = Wk.zbuf[u];
-              if (vjm) z = z - h1 * vjm[u];
-              z = z - h2 * vj[u];
-              Wk.zbuf[u] = z;
-              r[0] += dot4(z, z);
-            }
-            grid_reduce<1>(grid, sm, r, Wk.part);
-            ssz = r[0];
-          } else {
-            // generic modified Gram-Schmidt against the last `iom` vectors
-            const int64_t i0 = j - iom + 1 > 0 ? j - iom + 1 : 0;
-            double cprev = 0.0;
-            for (int64_t i = i0; i <= j + 1; ++i) {
-              const double4* vp = i > i0 ? Wk.basis + (i - 1) * NU : nullptr;
-              const double4* vi = i <= j ? Wk.basis + i * NU : nullptr;
-              double r[1] = {0.0};
-              for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-                double4 z = Wk.zbuf[u];
-                if (vp) {
-                  z = z - cprev * vp[u];
-                  Wk.zbuf[u] = z;
-                }
-                r[0] += vi ? dot4(vi[u], z) : dot4(z, z);
-              }
-              grid_reduce<1>(grid, sm, r, Wk.part);
-              if (i <= j) {
-                cprev = r[0];
-                if (lead) Wk.H[i * ld + j] = cprev;
-              } else {
-                ssz = r[0];
-              }
-            }
-          }
-          const double h = sqrt(ssz);
-          if (h < kBreakdownTol * beta) {
-            broke = true;
-            keep = j + 1;
-            hnext = 0.0;
-            break;
-          }
-          if (j + 1 < m_eff) {
-            // zbuf is complete: the reduction above ended with grid.sync
-            if (lead) Wk.H[(j + 1) * ld + j] = h;
-            hcur = h;
-            raw = Wk.zbuf;
-          } else {
-            hnext = h;
-          }
-        }
-        pc.mark(PC_KRYLOV);
-        // ---- dense phi via the augmented exponential (kernels.py:148-193)
-        __threadfence();
-        grid.sync();
-        if (blockIdx.x == 0) {
-          const int dim = (int)(keep + p + 1);
-          const DenseSmem ds = dense_smem(Wk.dsm_bytes);
-          const bool in_smem = ds.n >= 6 * dim * dim;
-          double* Mq[6];
-          for (int q = 0; q < 6; ++q)
-            Mq[q] = in_smem ? ds.p + (int64_t)q * dim * dim : Wk.scr + (int64_t)q * MAXDIM * MAXDIM;
-          const DenseSmem dsx = in_smem ? DenseSmem{nullptr, 0} : ds;
-          double* M0 = Mq[0];
-          for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) {
-            const int i = idx / dim, jj = idx - i * dim;
-            double hv = 0.0;
-            if (i < keep && jj < keep) hv = Wk.H[i * ld + jj];
-            else if (i == 0 && jj == keep) hv = 1.0;
-            else if (i >= keep && jj == i + 1 && i < keep + p) hv = 1.0;
-            M0[idx] = hv;  // Hhat
-          }
-          __syncthreads();
-          const double nrm_hat = blk_norm1(sm, M0, dim);
-          for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) M0[idx] = tau * M0[idx];
-          __syncthreads();
-          const double* E = blk_expm(sm, Mq, dim, dsx);
-          const double tp = pow(tau, (double)p);
-          const int colp = p >= 1 ? (int)keep + p - 1 : 0;
-          for (int i = threadIdx.x; i < keep; i += TPB) Wk.phi[i] = E[(int64_t)i * dim + colp] / tp;
-          if (threadIdx.x == 0) {
-            Wk.phi[keep] = E[(int64_t)(keep - 1) * dim + keep + p];
-            Wk.phi[keep + 1] = eik_mul(tau, nrm_hat);
-          }
-          __threadfence();
-        }
-        grid.sync();
-        for (int i = threadIdx.x; i < keep + 2; i += TPB) sm.phi[i] = __ldcg(Wk.phi + i);
-        __syncthreads();
-        corner = sm.phi[keep];
-        nh = sm.phi[keep + 1];
-        pc.mark(PC_DENSE);
-        eps = broke ? 0.0 : eik_mul(eik_mul(beta, fabs(hnext)), fabs(corner));
-      }
-
-      // ---- candidate (phipm.py:198-212, krylov.py:136-145)
-      double4* cand = Wk.ybuf[ycur == 0 ? 1 : 0];
-      {
-        double cj[MAXV];
-        for (int j = 0; j < p; ++j) cj[j] = pow_over_fact(tau, j);
-        const double tp = pow(tau, (double)p);
-        const double corr = (beta * hnext) * (corner / tp);
-        double r[1] = {0.0};
-        for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
-          double4 c = d4(0.0);
-          for (int j = 0; j < p; ++j) {
-            const double4 wv = (j == 0) ? y[u] : Wk.w[j][u];
-            c = c + cj[j] * wv;
-          }
-          if (wp_nz) {
-            double4 s = d4(0.0);
-            for (int64_t k = 0; k < keep; ++k) s = s + sm.phi[k] * Wk.basis[k * NU + u];
-            double4 ap = beta * s;
-            if (!broke) {
-              double4 zz = vnext_z[u];
-              if (!vnext_expl) {
-                if (vnext_m1) zz = zz - vnext_h1 * vnext_m1[u];
-                zz = zz - vnext_h2 * vnext_v[u];
-              }
-              ap = ap + corr * div4(zz, hnext);
-            }
-            c = c + tp * ap;
-          }
-          cand[u] = c;
-          r[0] += nz4(c);
-        }
-        grid_reduce<1>(grid, sm, r, Wk.part);
-        const bool cand_nz = r[0] > 0.0;
-        pc.mark(PC_CAND);
-
-        // ---- controller (phipm.py:336-359)
-        const double omega = eik_div(eik_mul(t_out, eps), eik_mul(tau, T.tol));
-        const bool ok = omega <= T.delta;
-        if (lead && Wk.trace && attempts <= Wk.trace_cap) {
-          EikTraceRec tr;
-          tr.attempt = attempts;
-          tr.t = t;
-          tr.tau = tau;
-          tr.m = m;
-          tr.eps_m = eps;
-          tr.omega = omega;
-          tr.accepted = ok ? 1 : 0;
-          Wk.trace[attempts - 1] = tr;
-          *Wk.trace_len = attempts;
-        }
-        const double tau_used = tau;
-        Adapt ad = adapt_parameters(tau, m, t, eps, nh, t_out, T.rho[T.ns - 1], p,
-                                    T.tol, T.delta, T.m_max, n, nnz);
-        if (ok) {
-          y = cand;
-          ycur = ycur == 0 ? 1 : 0;
-          y_nz = cand_nz;
-          t = hits ? t_out : eik_add(t, tau_used);
-          ++acc;
-          if (hits && ad.tau < tau_nom) ad.tau = tau_nom;
-        } else {
-          ++rej;
-        }
-        tau = ad.tau > 1e-16 ? ad.tau : 1e-16;
-        m = ad.m < 1 ? 1 : (ad.m > m_cap ? m_cap : ad.m);
+  ProfClock pc;
+  // ---- w recurrence (phipm.py:159-182)
+  const int p = E.p;
+  const unsigned vnzm = E.vnzm;
+  const double t = E.t;
+  const double4* wprev = E.y;
+  bool wprev_nz = E.y_nz != 0;
+  double ssq = 0.0;
+  int64_t mv = 0;
+  for (int j = 1; j <= p; ++j) {
+    double cl[MAXV];
+    for (int ell = 0; ell <= p - j; ++ell) cl[ell] = pow_over_fact(t, ell);
+    const bool do_mv = !(T.zero_skip && !wprev_nz);
+    double4* wj = Wk.w[j];
+    double r[2] = {0.0, 0.0};
+    bool tiled_mv = false;
+    if constexpr (Op::kTiled) tiled_mv = op.tiled_ok && do_mv;
+    if constexpr (Op::kTiled) {
+      if (tiled_mv) {
+        ++mv;
+        Form F{wprev, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+        swe_tiled(sm, op, F,
+                  [&](int64_t i, double4 z, double4, double4) {
+                    double4 a = z;
+                    for (int ell = 0; ell <= p - j; ++ell)
+                      if ((vnzm >> (j + ell)) & 1u) a = a + cl[ell] * T.v[j + ell][i];
+                    wj[i] = a;
+                    r[0] += nz4(a);
+                    r[1] += dot4(a, a);
+                  });
       }
     }
-    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) T.W[io][u] = y[u];
+    if (!tiled_mv) {
+      if (do_mv) {
+        op_pre(op, wprev, 1.0, lo, hi);
+        grid.sync();
+        ++mv;
+      }
+      for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+        double4 a = do_mv ? op_main(op, wprev, u) : d4(0.0);
+        for (int ell = 0; ell <= p - j; ++ell)
+          if ((vnzm >> (j + ell)) & 1u) a = a + cl[ell] * T.v[j + ell][u];
+        wj[u] = a;
+        r[0] += nz4(a);
+        r[1] += dot4(a, a);
+      }
+    }
+    grid_reduce<2>(grid, sm, r, Wk.part);
+    wprev = wj;
+    wprev_nz = r[0] > 0.0;
+    ssq = r[1];
   }
-  if (lead) {
+  if (p == 0) {
+    double r[2] = {0.0, 0.0};
+    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+      const double4 a = wprev[u];
+      r[0] += nz4(a);
+      r[1] += dot4(a, a);
+    }
+    grid_reduce<2>(grid, sm, r, Wk.part);
+    wprev_nz = r[0] > 0.0;
+    ssq = r[1];
+  }
+  E.wp = wprev;
+  E.wp_nz = wprev_nz ? 1 : 0;
+  pc.mark(PC_WREC);
+
+  // ---- IOM2 Krylov decomposition (krylov.py:53-112)
+  E.beta = 0.0;
+  E.hnext = 0.0;
+  E.broke = 0;
+  E.keep = 0;
+  // v_{m+1} = ((vz - h1 vm1) - h2 vv) / hnext (tiled sweep) or vz / hnext
+  E.vz = Wk.zbuf;
+  E.vm1 = nullptr;
+  E.vv = nullptr;
+  E.h1 = E.h2 = 0.0;
+  E.expl = 1;
+  if (!wprev_nz) {
+    E.mv = E.mv + mv;
+    return ER_CONTINUE;
+  }
+  const double beta = sqrt(ssq);
+  E.beta = beta;
+  const int64_t m_eff = E.m < n ? E.m : n;
+  const int64_t iom = m_eff < n ? T.iom : n;
+  E.m_eff = m_eff;
+  E.keep = m_eff;
+  if (blockIdx.x == 0) {
+    for (int64_t q = threadIdx.x; q < m_eff * ld; q += TPB) Wk.H[q] = 0.0;
+    __syncthreads();
+  }
+  if constexpr (Op::kTiled) {
+    if (iom == 2 && op.tiled_ok) {
+      E.mv = E.mv + mv;
+      return ER_SWEEP;
+    }
+  }
+  // generic operators: one matvec and one MGS pass per iteration
+  double hcur = beta;
+  const double4* raw = wprev;
+  for (int64_t j = 0; j < m_eff; ++j) {
+    double4* vj = Wk.basis + j * NU;
+    const double4* vjm = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
+    // v_j = raw / h (exact division), La = L v_j
+    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) vj[u] = div4(raw[u], hcur);
+    op_pre(op, raw, 1.0 / hcur, lo, hi);
+    grid.sync();
+    // z = A v_j + projections
+    double d[3] = {0.0, 0.0, 0.0};
+    const bool fast = (iom == 2);
+    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+      const double4 z = op_main(op, vj, u);
+      Wk.zbuf[u] = z;
+      if (fast) {
+        const double4 a = vj[u];
+        d[1] += dot4(a, z);
+        if (vjm) {
+          const double4 b = vjm[u];
+          d[0] += dot4(b, z);
+          d[2] += dot4(a, b);
+        }
+      }
+    }
+    ++mv;
+    if (lead) atomicAdd(Wk.kiters, 1ull);
+    double ssz = 0.0;
+    if (fast) {
+      grid_reduce<3>(grid, sm, d, Wk.part);
+      // MGS against v_{j-1} then v_j: <v_j, z - h1 v_{j-1}> = d1 - h1 d2
+      const double h1 = d[0];
+      const double h2 = vjm ? d[1] - h1 * d[2] : d[1];
+      if (lead) {
+        if (vjm) Wk.H[(j - 1) * ld + j] = h1;
+        Wk.H[j * ld + j] = h2;
+      }
+      double r[1] = {0.0};
+      for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+        double4 z = Wk.zbuf[u];
+        if (vjm) z = z - h1 * vjm[u];
+        z = z - h2 * vj[u];
+        Wk.zbuf[u] = z;
+        r[0] += dot4(z, z);
+      }
+      grid_reduce<1>(grid, sm, r, Wk.part);
+      ssz = r[0];
+    } else {
+      // generic modified Gram-Schmidt against the last `iom` vectors
+      const int64_t i0 = j - iom + 1 > 0 ? j - iom + 1 : 0;
+      double cprev = 0.0;
+      for (int64_t i = i0; i <= j + 1; ++i) {
+        const double4* vp = i > i0 ? Wk.basis + (i - 1) * NU : nullptr;
+        const double4* vi = i <= j ? Wk.basis + i * NU : nullptr;
+        double r[1] = {0.0};
+        for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+          double4 z = Wk.zbuf[u];
+          if (vp) {
+            z = z - cprev * vp[u];
+            Wk.zbuf[u] = z;
+          }
+          r[0] += vi ? dot4(vi[u], z) : dot4(z, z);
+        }
+        grid_reduce<1>(grid, sm, r, Wk.part);
+        if (i <= j) {
+          cprev = r[0];
+          if (lead) Wk.H[i * ld + j] = cprev;
+        } else {
+          ssz = r[0];
+        }
+      }
+    }
+    const double h = sqrt(ssz);
+    if (h < kBreakdownTol * beta) {
+      E.broke = 1;
+      E.keep = j + 1;
+      E.hnext = 0.0;
+      break;
+    }
+    if (j + 1 < m_eff) {
+      // zbuf is complete: the reduction above ended with grid.sync
+      if (lead) Wk.H[(j + 1) * ld + j] = h;
+      hcur = h;
+      raw = Wk.zbuf;
+    } else {
+      E.hnext = h;
+    }
+  }
+  E.mv = E.mv + mv;
+  pc.mark(PC_KRYLOV);
+  return ER_CONTINUE;
+}
+
+__device__ __forceinline__ void eng_store_sweep(ES& E, const KrylovState& ks, int64_t kmv) {
+  E.keep = ks.keep;
+  E.broke = ks.broke ? 1 : 0;
+  E.hnext = ks.hnext;
+  E.vz = ks.vz;
+  E.vm1 = ks.vm1;
+  E.vv = ks.vv;
+  E.h1 = ks.h1;
+  E.h2 = ks.h2;
+  E.expl = ks.expl ? 1 : 0;
+  E.mv = E.mv + kmv;
+  E.mode = EM_AFTER_SWEEP;
+}
+
+// Dense phi of the augmented Hessenberg matrix (kernels.py:148-193), the
+// candidate (phipm.py:198-212, krylov.py:136-145) and the step-size / order
+// controller (phipm.py:336-359).
+template <class Op>
+__device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
+                                   const EngineTask& T, const EngineWork& Wk, ES& E) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int64_t NU = Wk.NU, n = Wk.n, ld = Wk.m_alloc;
+  int64_t lo, hi;
+  brange(NU, lo, hi);
+  ProfClock pc;
+  const int p = E.p;
+  const double tau = E.tau;
+  const bool wp_nz = E.wp_nz != 0;
+  const bool broke = E.broke != 0;
+  const int64_t keep = E.keep;
+  const double beta = E.beta, hnext = E.hnext;
+  double eps = 0.0, nh = 0.0, corner = 0.0;
+  if (wp_nz) {
+    __threadfence();
+    grid.sync();
+    if (blockIdx.x == 0) {
+      const int dim = (int)(keep + p + 1);
+      const DenseSmem ds = dense_smem(Wk.dsm_bytes);
+      const bool in_smem = ds.n >= 6 * dim * dim;
+      double* Mq[6];
+      for (int q = 0; q < 6; ++q)
+        Mq[q] = in_smem ? ds.p + (int64_t)q * dim * dim : Wk.scr + (int64_t)q * MAXDIM * MAXDIM;
+      const DenseSmem dsx = in_smem ? DenseSmem{nullptr, 0} : ds;
+      double* M0 = Mq[0];
+      for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) {
+        const int i = idx / dim, jj = idx - i * dim;
+        double hv = 0.0;
+        if (i < keep && jj < keep) hv = Wk.H[i * ld + jj];
+        else if (i == 0 && jj == keep) hv = 1.0;
+        else if (i >= keep && jj == i + 1 && i < keep + p) hv = 1.0;
+        M0[idx] = hv;  // Hhat
+      }
+      __syncthreads();
+      const double nrm_hat = blk_norm1(sm, M0, dim);
+      for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) M0[idx] = tau * M0[idx];
+      __syncthreads();
+      const double* Ex = blk_expm(sm, Mq, dim, dsx);
+      const double tp = pow(tau, (double)p);
+      const int colp = p >= 1 ? (int)keep + p - 1 : 0;
+      for (int i = threadIdx.x; i < keep; i += TPB) Wk.phi[i] = Ex[(int64_t)i * dim + colp] / tp;
+      if (threadIdx.x == 0) {
+        Wk.phi[keep] = Ex[(int64_t)(keep - 1) * dim + keep + p];
+        Wk.phi[keep + 1] = eik_mul(tau, nrm_hat);
+      }
+      __threadfence();
+    }
+    grid.sync();
+    for (int i = threadIdx.x; i < keep + 2; i += TPB) sm.phi[i] = __ldcg(Wk.phi + i);
+    __syncthreads();
+    corner = sm.phi[keep];
+    nh = sm.phi[keep + 1];
+    pc.mark(PC_DENSE);
+    eps = broke ? 0.0 : eik_mul(eik_mul(beta, fabs(hnext)), fabs(corner));
+  }
+
+  // ---- candidate (phipm.py:198-212, krylov.py:136-145)
+  const int ycur = E.ycur;
+  double4* cand = Wk.ybuf[ycur == 0 ? 1 : 0];
+  bool cand_nz;
+  {
+    const double4* y = E.y;
+    const double4* vz = E.vz;
+    const double4* vm1 = E.vm1;
+    const double4* vv = E.vv;
+    const double h1 = E.h1, h2 = E.h2;
+    const bool expl = E.expl != 0;
+    double cj[MAXV];
+    for (int j = 0; j < p; ++j) cj[j] = pow_over_fact(tau, j);
+    const double tp = pow(tau, (double)p);
+    const double corr = (beta * hnext) * (corner / tp);
+    double r[1] = {0.0};
+    for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+      double4 c = d4(0.0);
+      for (int j = 0; j < p; ++j) {
+        const double4 wv = (j == 0) ? y[u] : Wk.w[j][u];
+        c = c + cj[j] * wv;
+      }
+      if (wp_nz) {
+        double4 s = d4(0.0);
+        for (int64_t k = 0; k < keep; ++k) s = s + sm.phi[k] * Wk.basis[k * NU + u];
+        double4 ap = beta * s;
+        if (!broke) {
+          double4 zz = vz[u];
+          if (!expl) {
+            if (vm1) zz = zz - h1 * vm1[u];
+            zz = zz - h2 * vv[u];
+          }
+          ap = ap + corr * div4(zz, hnext);
+        }
+        c = c + tp * ap;
+      }
+      cand[u] = c;
+      r[0] += nz4(c);
+    }
+    grid_reduce<1>(grid, sm, r, Wk.part);
+    cand_nz = r[0] > 0.0;
+  }
+  pc.mark(PC_CAND);
+
+  // ---- controller (phipm.py:336-359)
+  const double t = E.t, t_out = E.t_out;
+  const int64_t m = E.m, attempts = E.attempts;
+  const double omega = eik_div(eik_mul(t_out, eps), eik_mul(tau, T.tol));
+  const bool ok = omega <= T.delta;
+  if (lead && Wk.trace && attempts <= Wk.trace_cap) {
+    EikTraceRec tr;
+    tr.attempt = attempts;
+    tr.t = t;
+    tr.tau = tau;
+    tr.m = m;
+    tr.eps_m = eps;
+    tr.omega = omega;
+    tr.accepted = ok ? 1 : 0;
+    Wk.trace[attempts - 1] = tr;
+    *Wk.trace_len = attempts;
+  }
+  Adapt ad = adapt_parameters(tau, m, t, eps, nh, t_out, T.rho[T.ns - 1], p, T.tol, T.delta,
+                              T.m_max, n, E.nnz);
+  if (ok) {
+    const bool hits = E.hits != 0;
+    E.y = cand;
+    E.ycur = ycur == 0 ? 1 : 0;
+    E.y_nz = cand_nz ? 1 : 0;
+    E.t = hits ? t_out : eik_add(t, tau);
+    E.acc = E.acc + 1;
+    if (hits && ad.tau < E.tau_nom) ad.tau = E.tau_nom;
+  } else {
+    E.rej = E.rej + 1;
+  }
+  E.tau = ad.tau > 1e-16 ? ad.tau : 1e-16;
+  const int64_t m_cap = E.m_cap;
+  E.m = ad.m < 1 ? 1 : (ad.m > m_cap ? m_cap : ad.m);
+  E.mode = EM_ATTEMPT;
+}
+
+// Call summary and warm-start seeds (phipm.py:361-370).
+__device__ void eng_epilogue(cg::grid_group& grid, const EngineTask& T, const EngineWork& Wk,
+                             ES& E) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     EikPhipmInfo inf = {};
-    inf.substeps = acc;
-    inf.rejections = rej;
-    inf.matvecs = mv;
-    inf.tau_final = tau;
-    inf.m_final = m;
-    inf.t_reached = t;
-    inf.attempts = attempts;
+    inf.substeps = E.acc;
+    inf.rejections = E.rej;
+    inf.matvecs = E.mv;
+    inf.tau_final = E.tau;
+    inf.m_final = E.m;
+    inf.t_reached = E.t;
+    inf.attempts = E.attempts;
     inf.status = EIK_OK;
     Wk.info[T.info_idx] = inf;
     if (T.slot >= 0) {
-      Wk.seeds[2 * T.slot] = tau;
-      Wk.seeds[2 * T.slot + 1] = (double)m;
+      Wk.seeds[2 * T.slot] = E.tau;
+      Wk.seeds[2 * T.slot + 1] = (double)E.m;
     }
   }
   __threadfence();
   grid.sync();
-  return EIK_OK;
+}
+
+// One whole engine call in one kernel (the sweep inline); returns an
+// eik_status, uniformly in every CTA.
+template <class Op>
+__device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
+                           const EngineTask& T, const EngineWork& Wk, int64_t nnz) {
+  EngineState state;
+  ES& E = state;
+  if (!eng_prologue(grid, sm, T, Wk, nnz, E)) return EIK_OK;
+  for (;;) {
+    const int r = eng_attempt(grid, sm, op, T, Wk, E);
+    if (r == ER_DONE) {
+      eng_epilogue(grid, T, Wk, E);
+      return EIK_OK;
+    }
+    if (r == ER_FAIL) return EIK_EPHIPM;
+    if constexpr (Op::kTiled) {
+      if (r == ER_SWEEP) {
+        ProfClock pc;
+        int64_t kmv = 0;
+        const KrylovState ks = krylov_tiled(grid, sm, op, Wk, E.wp, E.beta, E.m_eff, kmv);
+        eng_store_sweep(E, ks, kmv);
+        pc.mark(PC_KRYLOV);
+      }
+    }
+    eng_finish_attempt(grid, sm, op, T, Wk, E);
+  }
 }
 
 }  // namespace eik
