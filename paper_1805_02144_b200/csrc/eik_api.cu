@@ -25,7 +25,7 @@ static thread_local std::string g_err;
 #endif
 // dynamic smem floor: the dense phase keeps its 6 matrices in shared memory
 // for n = m + p + 1 <= 46
-static constexpr size_t kDenseSmemBytes = 128 + (size_t)6 * 46 * 46 * 8;
+static constexpr size_t kDenseSmemBytes = 128 + (size_t)6 * 46 * dense_ld(46) * 8;
 static eik_status fail(eik_status s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
     in_engine = 1;
     __syncthreads();
     pc.skip();
-    if (E.mode == EM_AFTER_SWEEP) eng_finish_attempt(grid, sm, A.SD, sT, A.Wk, E);
+    if (E.mode == EM_AFTER_SWEEP) eng_finish_attempt(grid, sm, A.SD, sT, A.Wk, E, true);
   }
   for (;;) {
     if (!in_engine) {
@@ -497,6 +497,23 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
     }
     eng_finish_attempt(grid, sm, A.SD, sT, A.Wk, E);
   }
+}
+
+// The dense phase of an attempt after a sweep: one CTA of kDenseNT threads
+// with the matrices in shared memory (global scratch beyond ~68 x 68).
+__global__ void __launch_bounds__(kDenseNT, 1) k_swe_dense(SweArgs A) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ DenseRed rs;
+  if (threadIdx.x == 0) atomicAdd(A.Wk.kiters + 2, 1ull);
+  ProfClock pc;
+  const EngineState& E = A.ss->E;
+  if (E.mode != EM_AFTER_SWEEP || !E.wp_nz) return;
+  const int64_t keep = E.keep;
+  const int p = E.p;
+  const int dim = (int)(keep + p + 1);
+  double* buf = dense_fits_smem(dim) ? reinterpret_cast<double*>(dsm) : A.Wk.scr;
+  dense_phi<kDenseNT>(rs, A.Wk, buf, keep, p, E.tau);
+  pc.mark(PC_DENSE);
 }
 
 __global__ void __launch_bounds__(TPB, MINB) k_swe_sweep(SweArgs A) {
@@ -1399,15 +1416,25 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
 // k_swe_cont }  with the loop condition set on the device.  Monolithic
 // (EIK_STEP_MONO=1, or when the conditional graph cannot be built): one
 // k_swe_step launch.
-static bool capture_launches(cudaStream_t st, cudaGraph_t g, const void* const* fns,
-                             SweArgs* args, int nk, int G, size_t smem) {
+struct GraphLaunch {
+  const void* fn;
+  SweArgs* args;
+  bool coop;
+  int grid, block;
+  size_t smem;
+};
+
+static bool capture_launches(cudaStream_t st, cudaGraph_t g, const GraphLaunch* L, int nk) {
   if (cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0,
                                     cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return false;
   bool ok = true;
   for (int k = 0; k < nk && ok; ++k) {
-    void* kargs[] = {&args[k]};
-    ok = cudaLaunchCooperativeKernel(fns[k], G, TPB, kargs, smem, st) == cudaSuccess;
+    void* kargs[] = {L[k].args};
+    ok = (L[k].coop ? cudaLaunchCooperativeKernel(L[k].fn, L[k].grid, L[k].block, kargs,
+                                                  L[k].smem, st)
+                    : cudaLaunchKernel(L[k].fn, L[k].grid, L[k].block, kargs, L[k].smem, st)) ==
+         cudaSuccess;
   }
   cudaGraph_t out = g;
   ok = (cudaStreamEndCapture(st, &out) == cudaSuccess) && ok;
@@ -1419,18 +1446,29 @@ static bool build_step_graph(EikSwe* c, const SweArgs& A, bool split, cudaGraphE
   bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
   if (ok && !split) {
     SweArgs A0 = A;
-    const void* f0[] = {(const void*)k_swe_step};
-    ok = capture_launches(c->eng.st, g, f0, &A0, 1, c->eng.G, c->eng.smem);
+    const GraphLaunch L0[] = {{(const void*)k_swe_step, &A0, true, c->eng.G, TPB, c->eng.smem}};
+    ok = capture_launches(c->eng.st, g, L0, 1);
   } else if (ok) {
     cudaGraphConditionalHandle h = 0;
     ok = cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) == cudaSuccess;
-    SweArgs A0 = A, A1[2] = {A, A};
-    A0.cond = A1[0].cond = A1[1].cond = h;
+    SweArgs A0 = A, A1 = A;
+    A0.cond = A1.cond = h;
     A0.resume = 0;
-    A1[0].resume = A1[1].resume = 1;
-    const void* f0[] = {(const void*)k_swe_cont};
-    const void* f1[] = {(const void*)k_swe_sweep, (const void*)k_swe_cont};
-    ok = ok && capture_launches(c->eng.st, g, f0, &A0, 1, c->eng.G, c->eng.smem);
+    A1.resume = 1;
+    const int G = c->eng.G;
+    const size_t sm = c->eng.smem;
+    const GraphLaunch L0[] = {{(const void*)k_swe_cont, &A0, true, G, TPB, sm}};
+    const GraphLaunch L1[] = {{(const void*)k_swe_sweep, &A1, true, G, TPB, sm},
+                              {(const void*)k_swe_dense, &A1, false, 1, kDenseNT, kDenseKernelSmem},
+                              {(const void*)k_swe_cont, &A1, true, G, TPB, sm}};
+    static bool dense_attr = false;
+    if (!dense_attr) {
+      ok = ok && cudaFuncSetAttribute((const void*)k_swe_dense,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kDenseKernelSmem) == cudaSuccess;
+      dense_attr = ok;
+    }
+    ok = ok && capture_launches(c->eng.st, g, L0, 1);
     cudaGraphNode_t first = nullptr;
     size_t nn = 1;
     ok = ok && cudaGraphGetNodes(g, &first, &nn) == cudaSuccess && nn == 1;
@@ -1442,8 +1480,7 @@ static bool build_step_graph(EikSwe* c, const SweArgs& A, bool split, cudaGraphE
     cp.conditional.size = 1;
     cudaGraphNode_t cn = nullptr;
     ok = ok && cudaGraphAddNode(&cn, g, &first, 1, &cp) == cudaSuccess;
-    ok = ok && capture_launches(c->eng.st, cp.conditional.phGraph_out[0], f1, A1, 2, c->eng.G,
-                                c->eng.smem);
+    ok = ok && capture_launches(c->eng.st, cp.conditional.phGraph_out[0], L1, 3);
   }
   ok = ok && cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
   if (g) cudaGraphDestroy(g);

@@ -96,6 +96,33 @@ __device__ __forceinline__ double4 ld4(const double4* p, int64_t u) {
   return p ? p[u] : d4(0.0);
 }
 
+// 256-bit global accesses (one LDG/STG.E.ENL2.256 per cell instead of two
+// 128-bit halves hitting the same sector twice).  ldv: coherent (data written
+// earlier in the same kernel, ordered by a barrier); ldv_nc: read-only for the
+// kernel's lifetime.
+__device__ __forceinline__ double4 ldv(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double4 ldv_nc(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldv2_nc(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stv(double4* p, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
+               "d"(v.w)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- shared
 struct Smem {
   double red[NWARP][NPART];
@@ -900,30 +927,30 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
               b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
       if (va) {
-        a0 = F.src[ga];
-        if (F.vm2) a1 = F.vm2[ga];
-        if (F.vm1) a2 = F.vm1[ga];
-        if (ca < nE1) ua = S.lin[ga];
+        a0 = ldv(F.src + ga);
+        if (F.vm2) a1 = ldv(F.vm2 + ga);
+        if (F.vm1) a2 = ldv(F.vm1 + ga);
+        if (ca < nE1) ua = ldv_nc(S.lin + ga);
       }
       if (vb) {
-        b0 = F.src[gb];
-        if (F.vm2) b1 = F.vm2[gb];
-        if (F.vm1) b2 = F.vm1[gb];
-        if (cb < nE1) ub = S.lin[gb];
+        b0 = ldv(F.src + gb);
+        if (F.vm2) b1 = ldv(F.vm2 + gb);
+        if (F.vm1) b2 = ldv(F.vm1 + gb);
+        if (cb < nE1) ub = ldv_nc(S.lin + gb);
       }
       if (va) {
         const double4 x = form_x(F, a0, a1, a2);
         ts.gid[ca] = ga;
         sst(ts.x, ca, x);
         if (ca < nE1) sst(ts.U, ca, ua);
-        if (F.out && ca < nT) F.out[ga] = x;
+        if (F.out && ca < nT) stv(F.out + ga, x);
       }
       if (vb) {
         const double4 x = form_x(F, b0, b1, b2);
         ts.gid[cb] = gb;
         sst(ts.x, cb, x);
         if (cb < nE1) sst(ts.U, cb, ub);
-        if (F.out && cb < nT) F.out[gb] = x;
+        if (F.out && cb < nT) stv(F.out + gb, x);
       }
     }
     __syncthreads();
@@ -931,11 +958,14 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
     for (int c = threadIdx.x; c < nE1; c += TPB) {
       const Row8 row = load_row8(rows + (int64_t)c * 8);
       const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
+      const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(lc));
+      const double2 l45 = ldv2_nc(lc + 4);
+      const double lv[6] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y};
       const double4 xc = sld(ts.x, c);
       double4 acc = d4(0.0);
 #pragma unroll
       for (int s = 0; s < KCMAX; ++s) {
-        const double l = __ldg(lc + s);
+        const double l = lv[s];
         const double4 xv = sld(ts.x, row.s[s]);
         acc.x += l * (xv.x - xc.x);
         acc.y += l * (xv.y - xc.y);
@@ -953,12 +983,12 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       const double4 Ui = sld(ts.U, c);
       const double4 lai = sld(ts.La, c);
       const Row8 row = load_row8(rows + (int64_t)c * 8);
-      double lcr[8];
-#pragma unroll
-      for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(S.Lc + i * 8 + s);
+      const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(S.Lc + i * 8));
+      const double2 l45 = ldv2_nc(S.Lc + i * 8 + 4);
+      const double lcr[8] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y, 0.0, 0.0};
       const JvAcc a = swe_jv_part<0, KCMAX>(S, ts, row.s, lcr, 0, c, i, ai, Ui, lai);
-      const double4 z = S.scale * swe_jv_finish(S, a, S.ne[i], ai, Ui);
-      const double4 vm = F.epi_vm1 ? F.epi_vm1[i] : d4(0.0);
+      const double4 z = S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
+      const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
     }
     __syncthreads();
@@ -1021,131 +1051,89 @@ __device__ __forceinline__ double4 op_main(const CsrOp& C, const double4* x4,
 }
 
 // =================================================================== dense exp
-// Block-level degree-13 Pade with scaling and squaring (kernels.py:119-145),
-// run by one CTA on an L2-resident scratch; LU with partial pivoting
-// (LAPACK dgesv semantics: first max |pivot|, reciprocal scaling).
+// Block-level degree-13 Pade with scaling and squaring (kernels.py:119-145)
+// and LU with partial pivoting (LAPACK dgesv semantics: first max |pivot|,
+// reciprocal scaling), run by one CTA of NT threads.  Matrices are n x n,
+// row-major with a leading dimension ld = n rounded up to 4, plus 1,
+// in shared memory when they fit (the dedicated dense kernel) or else in the
+// L2-resident global scratch.  Every output of a product is one FMA chain
+// over k in ascending order, whatever the layout.
 
-// Dense scratch in shared memory for the single-CTA dense phase: the tile
-// buffers of the Krylov pass are dead by then (beyond the 128-byte header
-// that may hold the tile mbarriers).
-struct DenseSmem {
-  double* p;
-  int n;  // doubles available
+__host__ __device__ constexpr int dense_ld(int n) { return ((n + 3) & ~3) + 1; }  // = 1 mod 4
+
+struct DenseRed {
+  double red[32];
+  int ival;
 };
-__device__ __forceinline__ DenseSmem dense_smem(int64_t bytes) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  DenseSmem d;
-  d.p = reinterpret_cast<double*>(dsm + 128);
-  d.n = bytes > 256 ? (int)((bytes - 128) / 8) : 0;
-  return d;
-}
 
-constexpr int MMT = 32;  // dense matmul tile
-// C = A B (n x n, row-major, global/L2 scratch).  32x32 output tiles staged
-// through shared memory; each output is summed over k in ascending order.
-__device__ void blk_matmul(const double* A, const double* B, double* C, int n,
-                           const DenseSmem& ds) {
-  if (ds.n < 2 * MMT * (MMT + 1)) {
-    for (int idx = threadIdx.x; idx < n * n; idx += TPB) {
-      const int i = idx / n, j = idx - i * n;
-      const double* a = A + (int64_t)i * n;
-      double s = 0.0;
-      for (int k = 0; k < n; ++k) s += a[k] * B[(int64_t)k * n + j];
-      C[idx] = s;
+// C = A B; C must not alias A or B.  Thread -> 4 x 4 output block
+// (consecutive threads walk down the block rows, so with ld = 1 mod 4 the
+// four A-column loads of a warp are conflict-free and the B-row loads are
+// broadcasts); 16 FMA chains per thread, k ascending in each.
+template <int NT>
+__device__ void blk_matmul(const double* A, const double* B, double* C, int n, int ld) {
+  const int nb = (n + 3) >> 2;
+  for (int s = threadIdx.x; s < nb * nb; s += NT) {
+    const int bj = s / nb, bi = s - bj * nb;
+    const int i0 = 4 * bi, j0 = 4 * bj;
+    const int ni = min(4, n - i0), nj = min(4, n - j0);
+    const double* a = A + (int64_t)i0 * ld;
+    const double* b = B + j0;
+    double c[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[r][q] = 0.0;
+    for (int k = 0; k < n; ++k) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = r < ni ? a[(int64_t)r * ld + k] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = q < nj ? b[(int64_t)k * ld + q] : 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[r][q] += av[r] * bv[q];
     }
-    __syncthreads();
-    return;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (r < ni && q < nj) C[(int64_t)(i0 + r) * ld + j0 + q] = c[r][q];
   }
-  constexpr int EPT = (MMT * MMT + TPB - 1) / TPB;
-  double* As = ds.p;
-  double* Bs = ds.p + MMT * (MMT + 1);
-  const int nt = (n + MMT - 1) / MMT;
-  for (int ti = 0; ti < nt; ++ti)
-    for (int tj = 0; tj < nt; ++tj) {
-      double acc[EPT];
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) acc[e] = 0.0;
-      for (int tk = 0; tk < nt; ++tk) {
-        for (int e = threadIdx.x; e < MMT * MMT; e += TPB) {
-          const int r = e / MMT, c = e % MMT;
-          const int ia = ti * MMT + r, ka = tk * MMT + c;
-          const int kb = tk * MMT + r, jb = tj * MMT + c;
-          As[r * (MMT + 1) + c] = (ia < n && ka < n) ? A[(int64_t)ia * n + ka] : 0.0;
-          Bs[r * (MMT + 1) + c] = (kb < n && jb < n) ? B[(int64_t)kb * n + jb] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          const int idx = threadIdx.x + e * TPB;
-          if (idx < MMT * MMT) {
-            const int r = idx / MMT, c = idx % MMT;
-            double s = acc[e];
-            const int kmax = min(MMT, n - tk * MMT);
-            for (int k = 0; k < kmax; ++k) s += As[r * (MMT + 1) + k] * Bs[k * (MMT + 1) + c];
-            acc[e] = s;
-          }
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const int idx = threadIdx.x + e * TPB;
-        if (idx < MMT * MMT) {
-          const int i = ti * MMT + idx / MMT, j = tj * MMT + idx % MMT;
-          if (i < n && j < n) C[(int64_t)i * n + j] = acc[e];
-        }
-      }
-    }
   __syncthreads();
 }
 
 // max_j sum_i |M[i][j]|, rows summed in ascending order (numpy axis-0 reduce)
-__device__ double blk_norm1(Smem& sm, const double* M, int n) {
+template <int NT>
+__device__ double blk_norm1(DenseRed& rs, const double* M, int n, int ld) {
   double best = 0.0;
-  for (int j = threadIdx.x; j < n; j += TPB) {
+  for (int j = threadIdx.x; j < n; j += NT) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += fabs(M[(int64_t)i * n + j]);
+    for (int i = 0; i < n; ++i) s += fabs(M[(int64_t)i * ld + j]);
     best = fmax(best, s);
   }
-  // block max
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) sm.red[w][0] = best;
+  if (lane == 0) rs.red[w] = best;
   __syncthreads();
   double r = 0.0;
-  for (int q = 0; q < NWARP; ++q) r = fmax(r, sm.red[q][0]);
+  for (int q = 0; q < NT / 32; ++q) r = fmax(r, rs.red[q]);
   __syncthreads();
   return r;
 }
 
 // Solve P X = Q in place (Q <- X), P overwritten by its LU factors.
-__device__ void blk_solve_at(Smem& sm, double* P, double* Q, int n);
-__device__ void blk_solve(Smem& sm, double* P, double* Q, int n, const DenseSmem& ds) {
-  const int nn = n * n;
-  if (ds.n >= 2 * nn) {
-    double* Ps = ds.p;
-    double* Qs = ds.p + nn;
-    for (int idx = threadIdx.x; idx < nn; idx += TPB) {
-      Ps[idx] = P[idx];
-      Qs[idx] = Q[idx];
-    }
-    __syncthreads();
-    blk_solve_at(sm, Ps, Qs, n);
-    for (int idx = threadIdx.x; idx < nn; idx += TPB) Q[idx] = Qs[idx];
-    __syncthreads();
-  } else {
-    blk_solve_at(sm, P, Q, n);
-  }
-}
-__device__ void blk_solve_at(Smem& sm, double* P, double* Q, int n) {
+template <int NT>
+__device__ void blk_solve(DenseRed& rs, double* P, double* Q, int n, int ld) {
   for (int k = 0; k < n; ++k) {
     // pivot: first index of max |P[i][k]|, i >= k (warp 0)
     if (threadIdx.x < 32) {
       double best = -1.0;
       int bi = k;
       for (int i = k + threadIdx.x; i < n; i += 32) {
-        const double v = fabs(P[(int64_t)i * n + k]);
+        const double v = fabs(P[(int64_t)i * ld + k]);
         if (v > best) { best = v; bi = i; }
       }
 #pragma unroll
@@ -1154,69 +1142,59 @@ __device__ void blk_solve_at(Smem& sm, double* P, double* Q, int n) {
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
-      if (threadIdx.x == 0) sm.ival[0] = bi;
+      if (threadIdx.x == 0) rs.ival = bi;
     }
     __syncthreads();
-    const int piv = sm.ival[0];
+    const int piv = rs.ival;
     if (piv != k) {
-      for (int j = threadIdx.x; j < n; j += TPB) {
-        double t = P[(int64_t)k * n + j];
-        P[(int64_t)k * n + j] = P[(int64_t)piv * n + j];
-        P[(int64_t)piv * n + j] = t;
-        t = Q[(int64_t)k * n + j];
-        Q[(int64_t)k * n + j] = Q[(int64_t)piv * n + j];
-        Q[(int64_t)piv * n + j] = t;
+      for (int j = threadIdx.x; j < n; j += NT) {
+        double t = P[(int64_t)k * ld + j];
+        P[(int64_t)k * ld + j] = P[(int64_t)piv * ld + j];
+        P[(int64_t)piv * ld + j] = t;
+        t = Q[(int64_t)k * ld + j];
+        Q[(int64_t)k * ld + j] = Q[(int64_t)piv * ld + j];
+        Q[(int64_t)piv * ld + j] = t;
       }
       __syncthreads();
     }
-    const double pkk = P[(int64_t)k * n + k];
-    const double rinv = 1.0 / pkk;
-    for (int i = k + 1 + threadIdx.x; i < n; i += TPB) P[(int64_t)i * n + k] *= rinv;
+    const double rinv = 1.0 / P[(int64_t)k * ld + k];
+    for (int i = k + 1 + threadIdx.x; i < n; i += NT) P[(int64_t)i * ld + k] *= rinv;
     __syncthreads();
-    const int rows = n - k - 1;
-    const int width = (n - k - 1) + n;  // trailing P columns + all Q columns
-    for (int idx = threadIdx.x; idx < rows * width; idx += TPB) {
-      const int i = k + 1 + idx / width;
-      const int c = idx - (idx / width) * width;
-      const double l = P[(int64_t)i * n + k];
-      if (c < n - k - 1) {
-        const int j = k + 1 + c;
-        P[(int64_t)i * n + j] -= l * P[(int64_t)k * n + j];
-      } else {
-        const int j = c - (n - k - 1);
-        Q[(int64_t)i * n + j] -= l * Q[(int64_t)k * n + j];
-      }
+    // trailing update of P and Q: warp -> row, lane -> column
+    const int w0 = k + 1 - (k + 1) % 32;  // P columns from a 32-aligned start
+    for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+      const double l = P[(int64_t)i * ld + k];
+      for (int j = w0 + (int)(threadIdx.x & 31); j < n; j += 32)
+        if (j > k) P[(int64_t)i * ld + j] -= l * P[(int64_t)k * ld + j];
+      for (int j = threadIdx.x & 31; j < n; j += 32)
+        Q[(int64_t)i * ld + j] -= l * Q[(int64_t)k * ld + j];
     }
     __syncthreads();
   }
   // back substitution (dtrsm upper, non-unit)
   for (int k = n - 1; k >= 0; --k) {
-    const double pkk = P[(int64_t)k * n + k];
-    for (int j = threadIdx.x; j < n; j += TPB) Q[(int64_t)k * n + j] /= pkk;
+    const double pkk = P[(int64_t)k * ld + k];
+    for (int j = threadIdx.x; j < n; j += NT) Q[(int64_t)k * ld + j] /= pkk;
     __syncthreads();
-    for (int idx = threadIdx.x; idx < k * n; idx += TPB) {
-      const int i = idx / n, j = idx - i * n;
-      Q[(int64_t)i * n + j] -= Q[(int64_t)k * n + j] * P[(int64_t)i * n + k];
+    for (int i = (int)(threadIdx.x >> 5); i < k; i += NT / 32) {
+      const double pik = P[(int64_t)i * ld + k];
+      for (int j = threadIdx.x & 31; j < n; j += 32)
+        Q[(int64_t)i * ld + j] -= Q[(int64_t)k * ld + j] * pik;
     }
     __syncthreads();
   }
 }
 
-// E = expm(M0) for the n x n matrix in M0; returns the index of the scratch
-// matrix holding E.  scratch: 6 matrices of MAXDIM^2.
-// The matrices live in shared memory when 6 n^2 doubles fit (the common
-// case: n = m + p + 1 <= 46 with the SWE kernels' 102 KB dynamic smem),
-// else in the L2-resident global scratch `scr` (stride MAXDIM^2).  M[0]
-// holds the input on entry; returns the matrix holding exp(M[0]).
-__device__ double* blk_expm(Smem& sm, double** Mq, int n, const DenseSmem& ds) {
-  double* M[6];
-  for (int q = 0; q < 6; ++q) M[q] = Mq[q];
+// exp(M[0]) for the n x n matrix in M[0] (six matrices of n x ld scratch);
+// returns the matrix holding the result.
+template <int NT>
+__device__ double* blk_expm(DenseRed& rs, double* const* M, int n, int ld) {
   const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                         1187353796428800.0, 129060195264000.0, 10559470521600.0,
                         670442572800.0, 33522128640.0, 1323241920.0, 40840800.0,
                         960960.0, 16380.0, 182.0, 1.0};
-  const int nn = n * n;
-  const double nrm = blk_norm1(sm, M[0], n);
+  const int nn = n * ld;
+  const double nrm = blk_norm1<NT>(rs, M[0], n, ld);
   int s = 0;
   if (nrm > kPadeTheta) {
     const double c = ceil(log2(nrm / kPadeTheta));
@@ -1224,35 +1202,35 @@ __device__ double* blk_expm(Smem& sm, double** Mq, int n, const DenseSmem& ds) {
   }
   const double sc = ldexp(1.0, s);
   if (s > 0) {
-    for (int idx = threadIdx.x; idx < nn; idx += TPB) M[0][idx] = M[0][idx] / sc;
+    for (int idx = threadIdx.x; idx < nn; idx += NT) M[0][idx] = M[0][idx] / sc;
     __syncthreads();
   }
   double *X = M[0], *X2 = M[1], *X4 = M[2], *X6 = M[3];
-  blk_matmul(X, X, X2, n, ds);
-  blk_matmul(X2, X2, X4, n, ds);
-  blk_matmul(X2, X4, X6, n, ds);
+  blk_matmul<NT>(X, X, X2, n, ld);
+  blk_matmul<NT>(X2, X2, X4, n, ld);
+  blk_matmul<NT>(X2, X4, X6, n, ld);
   double* T = M[4];
-  for (int idx = threadIdx.x; idx < nn; idx += TPB)
+  for (int idx = threadIdx.x; idx < nn; idx += NT)
     T[idx] = b[13] * X6[idx] + b[11] * X4[idx] + b[9] * X2[idx];
   __syncthreads();
   double* T2 = M[5];
-  blk_matmul(X6, T, T2, n, ds);
-  for (int idx = threadIdx.x; idx < nn; idx += TPB) {
-    const int i = idx / n, j = idx - i * n;
+  blk_matmul<NT>(X6, T, T2, n, ld);
+  for (int idx = threadIdx.x; idx < nn; idx += NT) {
+    const int i = idx / ld, j = idx - i * ld;
     T2[idx] = T2[idx] + b[7] * X6[idx] + b[5] * X4[idx] + b[3] * X2[idx] +
               (i == j ? b[1] : 0.0);
   }
   __syncthreads();
   double* U = M[4];  // T is dead
-  blk_matmul(X, T2, U, n, ds);
+  blk_matmul<NT>(X, T2, U, n, ld);
   double* T3 = M[5];  // T2 is dead
-  for (int idx = threadIdx.x; idx < nn; idx += TPB)
+  for (int idx = threadIdx.x; idx < nn; idx += NT)
     T3[idx] = b[12] * X6[idx] + b[10] * X4[idx] + b[8] * X2[idx];
   __syncthreads();
   double* V = M[0];  // X is dead
-  blk_matmul(X6, T3, V, n, ds);
-  for (int idx = threadIdx.x; idx < nn; idx += TPB) {
-    const int i = idx / n, j = idx - i * n;
+  blk_matmul<NT>(X6, T3, V, n, ld);
+  for (int idx = threadIdx.x; idx < nn; idx += NT) {
+    const int i = idx / ld, j = idx - i * ld;
     const double v = V[idx] + b[6] * X6[idx] + b[4] * X4[idx] + b[2] * X2[idx] +
                      (i == j ? b[0] : 0.0);
     const double u = U[idx];
@@ -1260,10 +1238,10 @@ __device__ double* blk_expm(Smem& sm, double** Mq, int n, const DenseSmem& ds) {
     M[2][idx] = v + u;  // Q (X4 likewise)
   }
   __syncthreads();
-  blk_solve(sm, M[1], M[2], n, ds);
+  blk_solve<NT>(rs, M[1], M[2], n, ld);
   int cur = 2, oth = 3;
   for (int q = 0; q < s; ++q) {
-    blk_matmul(M[cur], M[cur], M[oth], n, ds);
+    blk_matmul<NT>(M[cur], M[cur], M[oth], n, ld);
     const int t = cur; cur = oth; oth = t;
   }
   return M[cur];
@@ -1304,6 +1282,51 @@ struct EngineWork {
   int64_t dsm_bytes;        // dynamic shared memory per CTA (dense phase scratch)
 };
 
+
+// phi coefficients of one attempt (phipm.py:186-196, kernels.py:148-193):
+// Hhat = [[H_keep, e_1, 0], [0, 0, I_{p-1}], [0, 0, 0]] of dimension
+// keep + p + 1, E = exp(tau Hhat); writes phi[i] = E[i][keep+p-1] / tau^p
+// (i < keep), phi[keep] = E[keep-1][keep+p] (the error corner) and
+// phi[keep+1] = tau ||Hhat||_1.  `buf`: 6 * dim * dense_ld(dim) doubles.
+template <int NT>
+__device__ void dense_phi(DenseRed& rs, const EngineWork& Wk, double* buf, int64_t keep, int p,
+                          double tau) {
+  const int dim = (int)(keep + p + 1);
+  const int ld = dense_ld(dim);
+  const int64_t ldh = Wk.m_alloc;
+  double* M[6];
+  for (int q = 0; q < 6; ++q) M[q] = buf + (int64_t)q * dim * ld;
+  double* M0 = M[0];
+  for (int idx = threadIdx.x; idx < dim * ld; idx += NT) {
+    const int i = idx / ld, jj = idx - i * ld;
+    double hv = 0.0;
+    if (i < keep && jj < keep) hv = Wk.H[i * ldh + jj];
+    else if (i == 0 && jj == keep) hv = 1.0;
+    else if (i >= keep && jj == i + 1 && i < keep + p) hv = 1.0;
+    M0[idx] = hv;  // Hhat (zero padding columns)
+  }
+  __syncthreads();
+  const double nrm_hat = blk_norm1<NT>(rs, M0, dim, ld);
+  for (int idx = threadIdx.x; idx < dim * ld; idx += NT) M0[idx] = tau * M0[idx];
+  __syncthreads();
+  const double* Ex = blk_expm<NT>(rs, M, dim, ld);
+  const double tp = pow(tau, (double)p);
+  const int colp = p >= 1 ? (int)keep + p - 1 : 0;
+  for (int i = threadIdx.x; i < keep; i += NT) Wk.phi[i] = Ex[(int64_t)i * ld + colp] / tp;
+  if (threadIdx.x == 0) {
+    Wk.phi[keep] = Ex[(int64_t)(keep - 1) * ld + keep + p];
+    Wk.phi[keep + 1] = eik_mul(tau, nrm_hat);
+  }
+  __threadfence();
+  __syncthreads();
+}
+
+// shared-memory budget of the dedicated dense kernel
+constexpr int kDenseNT = 1024;
+constexpr size_t kDenseKernelSmem = 220 * 1024;
+__host__ __device__ constexpr bool dense_fits_smem(int dim) {
+  return (size_t)6 * dim * dense_ld(dim) * 8 <= kDenseKernelSmem;
+}
 
 // Result of an IOM2 sweep: kept dimension, breakdown flag, h_{m+1,m} and the
 // recipe for v_{m+1} = ((vz - h1 vm1) - h2 vv) / hnext (or vz / hnext).
@@ -1363,7 +1386,7 @@ __device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp&
           swe_tiled(
               sm, op, F,
               [&](int64_t i, double4 z, double4 x, double4 b) {
-                zout[i] = z;
+                stv(zout + i, z);
                 d[1] += dot4(x, z);
                 d[3] += dot4(z, z);
                 d[4] += dot4(x, x);
@@ -1787,9 +1810,11 @@ __device__ __forceinline__ void eng_store_sweep(ES& E, const KrylovState& ks, in
 // Dense phi of the augmented Hessenberg matrix (kernels.py:148-193), the
 // candidate (phipm.py:198-212, krylov.py:136-145) and the step-size / order
 // controller (phipm.py:336-359).
+// dense_ready: phi already in Wk.phi (the split step's k_swe_dense).
 template <class Op>
 __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
-                                   const EngineTask& T, const EngineWork& Wk, ES& E) {
+                                   const EngineTask& T, const EngineWork& Wk, ES& E,
+                                   bool dense_ready = false) {
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   const int64_t NU = Wk.NU, n = Wk.n, ld = Wk.m_alloc;
   int64_t lo, hi;
@@ -1803,40 +1828,21 @@ __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
   const double beta = E.beta, hnext = E.hnext;
   double eps = 0.0, nh = 0.0, corner = 0.0;
   if (wp_nz) {
-    __threadfence();
-    grid.sync();
-    if (blockIdx.x == 0) {
-      const int dim = (int)(keep + p + 1);
-      const DenseSmem ds = dense_smem(Wk.dsm_bytes);
-      const bool in_smem = ds.n >= 6 * dim * dim;
-      double* Mq[6];
-      for (int q = 0; q < 6; ++q)
-        Mq[q] = in_smem ? ds.p + (int64_t)q * dim * dim : Wk.scr + (int64_t)q * MAXDIM * MAXDIM;
-      const DenseSmem dsx = in_smem ? DenseSmem{nullptr, 0} : ds;
-      double* M0 = Mq[0];
-      for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) {
-        const int i = idx / dim, jj = idx - i * dim;
-        double hv = 0.0;
-        if (i < keep && jj < keep) hv = Wk.H[i * ld + jj];
-        else if (i == 0 && jj == keep) hv = 1.0;
-        else if (i >= keep && jj == i + 1 && i < keep + p) hv = 1.0;
-        M0[idx] = hv;  // Hhat
-      }
-      __syncthreads();
-      const double nrm_hat = blk_norm1(sm, M0, dim);
-      for (int idx = threadIdx.x; idx < dim * dim; idx += TPB) M0[idx] = tau * M0[idx];
-      __syncthreads();
-      const double* Ex = blk_expm(sm, Mq, dim, dsx);
-      const double tp = pow(tau, (double)p);
-      const int colp = p >= 1 ? (int)keep + p - 1 : 0;
-      for (int i = threadIdx.x; i < keep; i += TPB) Wk.phi[i] = Ex[(int64_t)i * dim + colp] / tp;
-      if (threadIdx.x == 0) {
-        Wk.phi[keep] = Ex[(int64_t)(keep - 1) * dim + keep + p];
-        Wk.phi[keep + 1] = eik_mul(tau, nrm_hat);
-      }
+    if (!dense_ready) {
       __threadfence();
+      grid.sync();
+      if (blockIdx.x == 0) {
+        // the tile buffers are dead here: the matrices go to dynamic shared
+        // memory (past its 128-byte header) when they fit
+        extern __shared__ __align__(128) unsigned char dsm[];
+        __shared__ DenseRed rs;
+        const int dim = (int)(keep + p + 1);
+        const bool fits = (int64_t)6 * dim * dense_ld(dim) * 8 + 128 <= Wk.dsm_bytes;
+        double* buf = fits ? reinterpret_cast<double*>(dsm + 128) : Wk.scr;
+        dense_phi<TPB>(rs, Wk, buf, keep, p, tau);
+      }
+      grid.sync();
     }
-    grid.sync();
     for (int i = threadIdx.x; i < keep + 2; i += TPB) sm.phi[i] = __ldcg(Wk.phi + i);
     __syncthreads();
     corner = sm.phi[keep];

@@ -1,5 +1,6 @@
-for v in s256b2 s128b4 s128b3 s512b1 s256b1 s384b1 s256b2c2 s256b2c6; do
-  echo "== $v"; EIK_LIB=build/libeik_$v.so timeout 120 python tools/kbench.py C3 40 5 2>&1 | tail -1
+# usage: VARIANTS="a b" bash tools/vrun.sh   -- Krylov microbenchmark + step time per build/libeik_<v>.so
+for v in ${VARIANTS}; do
+  if [ "$v" = default ]; then L=""; else L="build/libeik_$v.so"; fi
+  echo "== $v"; EIK_LIB=$L timeout 120 python tools/kbench.py C3 40 5 2>&1 | tail -1
+  EIK_LIB=$L timeout 120 python tools/phases.py C3 6 2>&1 | head -1
 done
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>&1 | tail -1 | cut -c1-200
-for v in s256b2 s128b4 s256b1; do echo "== $v"; EIK_LIB=build/libeik_$v.so python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>&1 | tail -1 | cut -c1-200; done
