@@ -10,10 +10,14 @@ workload on its own GPU, with no data-path collective; ``value`` is the sum of
 steps over ranks divided by the max-over-ranks device time ("weak" scaling).
 
 A step is one EXPRB4 step of the resident state: F(u_n), eta, n_A, two
-phipm/IOM2 engine calls, the stage perturbation -- one cooperative kernel per
-step (libeik ``k_swe_step``), CUDA-graph replayed.  Timing: CUDA events
-recorded by libeik around every step kernel on its stream, barrier +
-device synchronise before and after the timed loop.  Each Krylov iteration
+phipm/IOM2 engine calls, the stage perturbation -- one CUDA graph per step
+(libeik's split step: a continuation kernel and, under a device-driven while
+node, one cooperative Krylov-sweep kernel ``k_swe_sweep`` per IOM2 sweep plus
+its dense phi kernel).  Timing: CUDA events recorded by libeik around every
+step graph on its stream, barrier + device synchronise before and after the
+timed loop.  The roofline is that of ``k_swe_sweep``, timed with CUDA events
+around each sweep launch in a second pass of the same steps launched kernel by
+kernel (host-loop mode: conditional graph nodes hide their kernels).  Each Krylov iteration
 streams ~0.5 GB, far more than the 126 MB L2, so no explicit flush is done.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
@@ -50,6 +54,7 @@ def parse():
     ap.add_argument("--scheme", default="exprb42")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sweep-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -251,21 +256,36 @@ def main():
     e2e_wall = time.perf_counter() - te
     e2e, _ = aggregate_throughput(args.e2e_steps, 1e3 * e2e_wall, dist, f"cuda:{local}")
 
+    # the dominant kernel alone: the same steps launched kernel by kernel
+    # (host-loop mode, identical results), every Krylov sweep kernel
+    # bracketed by CUDA events on the libeik stream
+    ctx.set_hostloop(True)
+    ctx.sweep_timing(reset=True)
+    k1 = ctx.krylov_iters()
+    for _ in range(max(1, min(args.steps, args.sweep_steps))):
+        step()
+    torch.cuda.synchronize(local)
+    sweep_ms, nsweeps = ctx.sweep_timing(reset=True)
+    sweep_iters = ctx.krylov_iters() - k1
+    ctx.set_hostloop(False)
+
     hbm, src = peaks()
     balg = b_alg_per_iter(ops)
     it_per_step = kiters / args.steps
-    # algorithmic bytes of the step kernel's dominant work: every J*v pass
-    # (Krylov iterations and w-recurrence matvecs) at B_alg, plus the
-    # candidate update reading each kept basis vector once (32 B/cell)
+    # roofline of k_swe_sweep: algorithmic bytes per launch (B_alg x the
+    # launch's Krylov iterations) / average launch duration
+    achieved = balg * sweep_iters / (sweep_ms / 1e3) / 1e9
+    iters_per_launch = sweep_iters / max(nsweeps, 1)
+    # whole step: every J*v pass at B_alg + the candidate's basis reads
     step_bytes = balg * mv + 32.0 * ops.n_g * kiters
-    achieved = step_bytes / (dev_ms / 1e3) / 1e9
+    step_achieved = step_bytes / (dev_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
             tr = json.load(fh)
-        if tr.get("cells") == ops.n_g:
-            traffic = tr["dram_bytes_per_jv"] * (mv / args.steps)
+        if tr.get("cells") == ops.n_g and tr.get("kernel") == "k_swe_sweep":
+            traffic = tr["dram_bytes_per_iter"] * iters_per_launch
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -283,11 +303,20 @@ def main():
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "note": f"kernel = whole-step k_swe_step (one launch per step); achieved "
-                             f"= (B_alg {balg / 1e6:.1f} MB x J*v passes + 32 B/cell x Krylov "
-                             f"iters) / step-kernel time, per launch; traffic = ncu DRAM "
-                             f"bytes per J*v pass (profiles/traffic.json) x J*v passes per "
-                             f"step; peak {src} (MEASURED_PEAKS.json hbm_gbs)"},
+                     "kernel": "k_swe_sweep",
+                     "launches": nsweeps, "iters_per_launch": iters_per_launch,
+                     "us_per_iter": 1e3 * sweep_ms / max(sweep_iters, 1),
+                     "sweep_share_of_step": (sweep_ms / max(1, min(args.steps, args.sweep_steps))) / ms_per_step,
+                     "step_achieved": step_achieved, "step_frac": step_achieved / hbm,
+                     "note": f"kernel = k_swe_sweep (one IOM2 Krylov sweep per launch, "
+                             f"{iters_per_launch:.1f} iterations avg); achieved = B_alg "
+                             f"{balg / 1e6:.1f} MB x iterations / CUDA-event time of the "
+                             f"sweep launches ({nsweeps} launches over "
+                             f"{max(1, min(args.steps, args.sweep_steps))} steps in host-loop "
+                             f"mode); traffic = ncu DRAM bytes per iteration of one captured "
+                             f"launch (profiles/traffic.json) x iterations per launch; "
+                             f"step_* = every J*v pass + candidate reads over the whole "
+                             f"graph-replayed step; peak {src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * 4 * ops.n_g,
                 "d2h_bytes_per_step": 8 * 4 * ops.n_g},
         "gpu_launches": launches,

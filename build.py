@@ -30,7 +30,7 @@ def build(force=False, verbose=False, out=OUT, defines=()):
         return OUT
     cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp", *SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(ROOT, "build", "ptxas.log")
+    log = os.path.join(ROOT, "build", "ptxas.log" if out == OUT else os.path.basename(out) + ".ptxas.log")
     os.makedirs(os.path.dirname(log), exist_ok=True)
     with open(log, "w") as fh:
         fh.write(r.stdout + r.stderr)
@@ -40,7 +40,7 @@ def build(force=False, verbose=False, out=OUT, defines=()):
     os.replace(out + ".tmp", out)
     if verbose:
         print(r.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

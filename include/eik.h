@@ -175,6 +175,16 @@ int eik_prof_read(double* out, int reset);
 int64_t eik_swe_launches(const EikSwe* ctx);
 /* last step's per-phase device time in ms (CUDA events), engine-kernel only */
 double eik_swe_last_kernel_ms(const EikSwe* ctx);
+/* host-loop mode (on != 0): eik_swe_step launches the split step's kernels
+ * one by one instead of replaying its CUDA graph (conditional graph nodes
+ * cannot be profiled by ncu), reading the loop condition back after every
+ * continuation kernel and bracketing every Krylov sweep kernel with CUDA
+ * events.  Results are identical; it is slower (one host sync per sweep).
+ * Also selected by the environment variable EIK_STEP_HOST at creation. */
+eik_status eik_swe_set_hostloop(EikSwe* ctx, int32_t on);
+/* total device time (ms, CUDA events) and number of the Krylov sweep kernels
+ * run in host-loop mode since the last reset; reset != 0 zeroes them */
+eik_status eik_swe_sweep_timing(EikSwe* ctx, double* ms, int64_t* nsweeps, int32_t reset);
 /* Krylov iterations (IOM2 J*v) performed since creation */
 int64_t eik_swe_krylov_iters(const EikSwe* ctx);
 /* of those, iterations that needed the explicit orthogonalisation pass

@@ -83,6 +83,8 @@ _SIGS = {
     "eik_prof_read": (C.c_int, [_D, C.c_int]),
     "eik_swe_launches": (C.c_int64, [_P]),
     "eik_swe_last_kernel_ms": (C.c_double, [_P]),
+    "eik_swe_set_hostloop": (C.c_int, [_P, C.c_int32]),
+    "eik_swe_sweep_timing": (C.c_int, [_P, _D, C.POINTER(C.c_int64), C.c_int32]),
     "eik_swe_krylov_iters": (C.c_int64, [_P]),
     "eik_swe_explicit_orth": (C.c_int64, [_P]),
     "eik_csr_create": (C.c_int, [C.c_int32, EikCsrView, C.c_int32, C.c_int32,

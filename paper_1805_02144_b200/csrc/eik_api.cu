@@ -71,7 +71,8 @@ struct alignas(8) StepState {
   int64_t nA;
   const double4* base;
   const double4* fin;
-  int call, pad;
+  int call;
+  int more;  // host-loop mode: the loop condition (the graph uses `cond`)
 };
 
 struct SweArgs {
@@ -93,6 +94,7 @@ struct SweArgs {
   StepState* ss;                    // saved step position (global)
   cudaGraphConditionalHandle cond;  // loop condition of the graph's while node
   int resume;                       // 0: first k_swe_cont of the step
+  int hostloop;                     // 1: no graph; the host reads ss->more
 };
 
 // F(w) (+ eta at w when `lin` is w); optional out_v = dt * F.
@@ -409,7 +411,10 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
 // whole register budget and no controller state live across it.
 __device__ void cont_stop(const SweArgs& A, int st) {
   set_status(A.status, st);
-  if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(A.cond, 0u);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (A.hostloop) A.ss->more = 0;
+    else cudaGraphSetConditional(A.cond, 0u);
+  }
 }
 
 __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
@@ -484,7 +489,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
         G->base = base;
         G->fin = fin;
         G->call = call;
-        cudaGraphSetConditional(A.cond, 1u);
+        if (A.hostloop) G->more = 1;
+        else cudaGraphSetConditional(A.cond, 1u);
       }
       return;
     }
@@ -884,6 +890,15 @@ struct EikSwe {
   bool split = getenv("EIK_STEP_MONO") == nullptr;  // split step graph
   StepState* ss = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // host-loop mode (no graph): the split step's kernels launched one by one,
+  // the loop condition read back after every k_swe_cont; every Krylov sweep
+  // is bracketed by CUDA events (sweep-kernel timing, ncu profiling)
+  bool hostloop = getenv("EIK_STEP_HOST") != nullptr;
+  cudaEvent_t evs0 = nullptr, evs1 = nullptr;
+  double sweep_ms = 0.0;
+  int64_t nsweeps = 0;
+  bool sweep_log = getenv("EIK_SWEEP_LOG") != nullptr;
+  unsigned long long kit_last = 0;
   float last_ms = 0.0f;
   double* pinned = nullptr;  // pinned staging for host copies (4N doubles)
 
@@ -1053,7 +1068,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   KC = std::min(KC, KCMAX);
   for (int64_t i = 0; i < N; ++i)
     for (int q = offc[i]; q < KMAX; ++q) offn[(size_t)q * N + i] = (int32_t)i;
-  std::vector<double> coefc((size_t)KCMAX * 9 * N, 0.0);
+  const int64_t NC = (N + 1) & ~(int64_t)1;  // even run stride: 16-byte aligned TMA runs
+  std::vector<double> coefc((size_t)KCMAX * 9 * NC + 2, 0.0);
   std::vector<double> Lc((size_t)N * 8, 0.0);
   // compact op order: Vx Vy Vz Gx Gy Gz Dx Dy Dz
   const int corder[9] = {OP_VX, OP_VY, OP_VZ, OP_GX, OP_GY, OP_GZ, OP_DX, OP_DY, OP_DZ};
@@ -1062,7 +1078,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
     for (int s2 = 0; s2 < cnt[i] && q < KC; ++s2) {
       if (cols[i][s2] == i) continue;
       for (int k = 0; k < 9; ++k)
-        coefc[((size_t)q * 9 + k) * N + i] = coef[((size_t)s2 * NOPS + corder[k]) * N + i];
+        coefc[((size_t)q * 9 + k) * NC + i] = coef[((size_t)s2 * NOPS + corder[k]) * N + i];
       Lc[(size_t)i * 8 + q] = coef[((size_t)s2 * NOPS + OP_L) * N + i];
       ++q;
     }
@@ -1075,14 +1091,34 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
     return fail(EIK_ECUDA, "no CUDA device");
   const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * MINB, (N + TILE - 1) / TILE));
-  const int64_t per = (N + (int64_t)Gt * TILE - 1) / ((int64_t)Gt * TILE);
-  const int NT = (int)(Gt * per);
-  int64_t tsz = (N + NT - 1) / NT;
-  if (tsz & 1) ++tsz;  // even tiles keep the TMA runs 16-byte aligned
-  std::vector<int32_t> t_cell0(NT), t_nT(NT), t_nE1(NT), t_nE2(NT), t_e2off(NT), t_e1off(NT);
+  // the tile buffers of MINB co-resident CTAs must fit one SM's shared
+  // memory: shrink the tiles (more per CTA) until they do
+  int smem_sm = 0, smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const size_t smem_budget =
+      std::min<size_t>((size_t)smem_optin, (size_t)smem_sm / MINB - 1024 - 4096);
+  int NT = 0;
+  int64_t tsz = 0;
+  std::vector<int32_t> t_cell0, t_nT, t_nE1, t_nE2, t_e2off, t_e1off;
   std::vector<int32_t> e2map;
   std::vector<int16_t> lnbr;
+  std::vector<double> LcE1;  // Laplacian rows of every tile's E1 cells, local order
   int e1max = 1, e2max = 1;
+#ifndef EIK_TILE_CAP
+#define EIK_TILE_CAP TILE
+#endif
+  constexpr int64_t kTileCap = EIK_TILE_CAP;  // own cells per tile (<= TILE)
+  static_assert(kTileCap <= TILE, "tile cap");
+  for (int64_t per = (N + (int64_t)Gt * kTileCap - 1) / ((int64_t)Gt * kTileCap);; ++per) {
+  NT = (int)(Gt * per);
+  tsz = (N + NT - 1) / NT;
+  if (tsz & 1) ++tsz;  // even tiles keep the TMA runs 16-byte aligned
+  for (auto* v : {&t_cell0, &t_nT, &t_nE1, &t_nE2, &t_e2off, &t_e1off}) v->assign(NT, 0);
+  e2map.clear();
+  lnbr.clear();
+  LcE1.clear();
+  e1max = e2max = 1;
   {
     std::vector<int32_t> loc(N, -1), list;
     for (int t = 0; t < NT; ++t) {
@@ -1114,11 +1150,15 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
           const int32_t j = q < KMAX ? offn[(size_t)q * N + gi] : gi;
           lnbr.push_back((int16_t)loc[j]);
         }
+        for (int q = 0; q < KCMAX; ++q) LcE1.push_back(Lc[(size_t)gi * 8 + q]);
       }
       for (int32_t g2 : list) { e2map.push_back(g2); loc[g2] = -1; }
+      while (e2map.size() & 3) e2map.push_back(0);  // 16-byte aligned per-tile runs
       e1max = std::max(e1max, nE1);
       e2max = std::max(e2max, nE2);
     }
+  }
+  if (tile_smem_bytes(e1max, e2max) <= smem_budget || tsz <= 2) break;
   }
   // ---- balance: tile t is processed by CTA t % Gt in the kernels; permute
   // the tiles so that this static assignment is a longest-processing-time
@@ -1212,6 +1252,9 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&d_lnbr, lnbr.size()));
   CKC(B.get(&d_Lc, Lc.size()));
   double* d_coefc;
+  double* d_LcE1;
+  CKC(B.get(&d_LcE1, LcE1.size() + 2));
+  CKC(cudaMemcpy(d_LcE1, LcE1.data(), LcE1.size() * 8, cudaMemcpyHostToDevice));
   CKC(B.get(&d_coefc, coefc.size()));
   CKC(cudaMemcpy(d_coefc, coefc.data(), coefc.size() * 8, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_tc0, t_cell0.data(), NTb * 4, cudaMemcpyHostToDevice));
@@ -1247,6 +1290,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&lapB, N));
   CKC(cudaEventCreate(&c->ev0));
   CKC(cudaEventCreate(&c->ev1));
+  CKC(cudaEventCreate(&c->evs0));
+  CKC(cudaEventCreate(&c->evs1));
 #undef CKC
   SweOp& S = c->S;
   S.N = N;
@@ -1276,6 +1321,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.lnbr = d_lnbr;
   S.Lc = d_Lc;
   S.coefc = d_coefc;
+  S.NC = NC;
+  S.LcE1 = d_LcE1;
   S.KC = KC;
   S.tiled_ok = tiled_ok ? 1 : 0;
   S.prof = nullptr;
@@ -1294,6 +1341,8 @@ eik_status eik_swe_destroy(EikSwe* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->evs0) cudaEventDestroy(c->evs0);
+  if (c->evs1) cudaEventDestroy(c->evs1);
   c->eng.release();
   delete c;
   return EIK_OK;
@@ -1424,6 +1473,15 @@ struct GraphLaunch {
   size_t smem;
 };
 
+static bool dense_attr_set() {
+  static bool done = false;
+  if (!done)
+    done = cudaFuncSetAttribute((const void*)k_swe_dense,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kDenseKernelSmem) == cudaSuccess;
+  return done;
+}
+
 static bool capture_launches(cudaStream_t st, cudaGraph_t g, const GraphLaunch* L, int nk) {
   if (cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0,
                                     cudaStreamCaptureModeThreadLocal) != cudaSuccess)
@@ -1461,13 +1519,7 @@ static bool build_step_graph(EikSwe* c, const SweArgs& A, bool split, cudaGraphE
     const GraphLaunch L1[] = {{(const void*)k_swe_sweep, &A1, true, G, TPB, sm},
                               {(const void*)k_swe_dense, &A1, false, 1, kDenseNT, kDenseKernelSmem},
                               {(const void*)k_swe_cont, &A1, true, G, TPB, sm}};
-    static bool dense_attr = false;
-    if (!dense_attr) {
-      ok = ok && cudaFuncSetAttribute((const void*)k_swe_dense,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kDenseKernelSmem) == cudaSuccess;
-      dense_attr = ok;
-    }
+    ok = ok && dense_attr_set();
     ok = ok && capture_launches(c->eng.st, g, L0, 1);
     cudaGraphNode_t first = nullptr;
     size_t nn = 1;
@@ -1491,12 +1543,55 @@ static bool build_step_graph(EikSwe* c, const SweArgs& A, bool split, cudaGraphE
   return ok;
 }
 
+// The split step without a graph: cont ; while (ss->more) { sweep ; dense ; cont }.
+static eik_status step_hostloop(EikSwe* c, SweArgs A) {
+  if (!dense_attr_set()) return fail(EIK_ECUDA, "k_swe_dense shared-memory attribute");
+  A.hostloop = 1;
+  A.cond = 0;
+  A.resume = 0;
+  if (c->sweep_log)
+    CK(cudaMemcpy(&c->kit_last, c->eng.kiters_d, sizeof(c->kit_last), cudaMemcpyDeviceToHost));
+  // (launch counts: these kernels count themselves on the device)
+  void* kargs[] = {&A};
+  const int G = c->eng.G;
+  const size_t sm = c->eng.smem;
+  CK(cudaLaunchCooperativeKernel((const void*)k_swe_cont, G, TPB, kargs, sm, c->eng.st));
+  A.resume = 1;
+  for (;;) {
+    int more = 0;
+    CK(cudaMemcpyAsync(&more, &c->ss->more, sizeof(int), cudaMemcpyDeviceToHost, c->eng.st));
+    CK(cudaStreamSynchronize(c->eng.st));
+    if (!more) break;
+    CK(cudaEventRecord(c->evs0, c->eng.st));
+    CK(cudaLaunchCooperativeKernel((const void*)k_swe_sweep, G, TPB, kargs, sm, c->eng.st));
+    CK(cudaEventRecord(c->evs1, c->eng.st));
+    CK(cudaLaunchKernel((const void*)k_swe_dense, 1, kDenseNT, kargs, kDenseKernelSmem,
+                        c->eng.st));
+    CK(cudaLaunchCooperativeKernel((const void*)k_swe_cont, G, TPB, kargs, sm, c->eng.st));
+    CK(cudaEventSynchronize(c->evs1));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, c->evs0, c->evs1));
+    c->sweep_ms += ms;
+    if (c->sweep_log) {
+      // per-sweep record for matching ncu captures (launch index, iterations)
+      unsigned long long kit = 0;
+      CK(cudaMemcpy(&kit, c->eng.kiters_d, sizeof(kit), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[eik] sweep %lld iters %llu ms %.4f\n", (long long)c->nsweeps,
+              kit - c->kit_last, ms);
+      c->kit_last = kit;
+    }
+    ++c->nsweeps;
+  }
+  return EIK_OK;
+}
+
 static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol) {
   SweArgs A = c->args(c->u, dt);
   A.dt = dt;
   A.tol = tol;
   A.scheme = scheme;
   A.ss = c->ss;
+  if (c->hostloop) return step_hostloop(c, A);
   if (c->graphs_ok) {
     if (!c->gexec || c->g_scheme != scheme || c->g_dt != dt || c->g_tol != tol) {
       if (c->gexec) {
@@ -1687,6 +1782,21 @@ int64_t eik_swe_launches(const EikSwe* c) {
   return c->eng.launches + (int64_t)v[2];
 }
 double eik_swe_last_kernel_ms(const EikSwe* c) { return c ? (double)c->last_ms : 0.0; }
+eik_status eik_swe_set_hostloop(EikSwe* c, int32_t on) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  c->hostloop = on != 0;
+  return EIK_OK;
+}
+eik_status eik_swe_sweep_timing(EikSwe* c, double* ms, int64_t* nsweeps, int32_t reset) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  if (ms) *ms = c->sweep_ms;
+  if (nsweeps) *nsweeps = c->nsweeps;
+  if (reset) {
+    c->sweep_ms = 0.0;
+    c->nsweeps = 0;
+  }
+  return EIK_OK;
+}
 int64_t eik_swe_krylov_iters(const EikSwe* c) {
   if (!c) return 0;
   unsigned long long v = 0;

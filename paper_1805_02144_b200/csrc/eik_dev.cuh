@@ -239,8 +239,11 @@ struct SweOp {
   const int* t_e1off;    // offset into lnbr (rows)
   const int* e2map;      // local -> global cell id, order [own, H1, H2]
   const short* lnbr;     // [rows][8] local off-diagonal neighbours of E1 cells
-  const double* coefc;   // [KC][9][N] off-diagonal G, D, V (compact stencil)
+  const double* coefc;   // [KC][9][NC] off-diagonal G, D, V (compact stencil)
+  int64_t NC;            // coefficient run stride (N rounded up to even: 16-byte runs)
   const double* Lc;      // [N][8] off-diagonal Laplacian row (cell-major)
+  const double* LcE1;    // [sum of tile E1][6] Laplacian rows of every tile's E1 cells
+                         // in local order (offset t_e1off * 6)
   int KC;                // off-diagonal slots
   int tiled_ok;          // compact stencil valid for this operator set
   unsigned long long* prof;  // EIK_PROF builds: per-step cycle counters
@@ -381,9 +384,22 @@ constexpr int WS = EIK_WS;
 #ifndef EIK_WS_TPC
 #define EIK_WS_TPC 1
 #endif
+// EIK_SR2 (default): the single-role pass with its per-tile static data
+// (coefficients, n/eta, Laplacian rows and local neighbour rows of the
+// 1-ring) bulk-copied into shared memory by TMA while the threads gather
+// the halo, the next tile's cell map prefetched one tile ahead, and
+// EIK_SR2_TPC threads per own cell in the J v step.
+#ifndef EIK_SR2
+#define EIK_SR2 0
+#endif
+#ifndef EIK_SR2_TPC
+#define EIK_SR2_TPC 2
+#endif
+constexpr int SR2 = (EIK_WS == 0) ? EIK_SR2 : 0;
+constexpr int SR2_TPC = EIK_SR2_TPC;
 constexpr int PT = EIK_PT;                       // producer threads (TMA warp + gatherers)
 constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell
-constexpr int TILE = WS ? (TPB - PT) / WS_TPC : TPB;  // max own cells per tile
+constexpr int TILE = WS ? (TPB - PT) / WS_TPC : (SR2 ? TPB / SR2_TPC : TPB);  // max own cells per tile
 static_assert(WS != 2 || TILE == 256, "TMA-WS: 256-cell tiles");
 #ifndef EIK_PROF
 #define EIK_PROF 0
@@ -417,16 +433,48 @@ __device__ __forceinline__ void sst(const SArr& a, int l, double4 v) {
 #endif
 }
 
+#ifndef EIK_LCE1
+#define EIK_LCE1 1
+#endif
+#ifndef EIK_VMB
+#define EIK_VMB 0
+#endif
+#ifndef EIK_PRE3
+#define EIK_PRE3 0
+#endif
+#ifndef EIK_CPA
+#define EIK_CPA 0
+#endif
+#ifndef EIK_L2PF
+#define EIK_L2PF 0
+#endif
+#ifndef EIK_PIPE3
+#define EIK_PIPE3 0
+#endif
 struct TileSmem {
   double* cb;  // [NCOEF][TILE] staged own-cell coefficients (TMA pipeline) or null
   SArr x;
   SArr La;
   SArr U;
   int* gid;
+  double4* vmb;  // [TILE] own-cell vector for the epilogue (EIK_VMB)
+  // EIK_CPA: per-tile static data staged by cp.async
+  short* rows;   // [e1max][8] local neighbour rows of E1
+  double* lce1;  // [e1max][6] Laplacian rows of E1
+  double4* neb;  // [TILE] (n, eta) of the own cells
+  int* map0;     // [e2r] cell map, double-buffered (next tile's prefetched)
+  int* map1;
 };
 
+__host__ __device__ constexpr int e2_round4(int e2max) { return (e2max + 3) & ~3; }
+#ifndef EIK_SMEM_PAD
+#define EIK_SMEM_PAD 0
+#endif
 __host__ __device__ constexpr size_t tile_buf_bytes(int e1max, int e2max) {
-  return (size_t)e2max * 32 + (size_t)e1max * 64 + (size_t)e2max * 4 + 16;
+  return (size_t)EIK_SMEM_PAD + (size_t)(EIK_VMB ? TILE : 0) * 32 + (size_t)e2max * 32 +
+         (size_t)e1max * 64 + (size_t)(EIK_LCE1 && !EIK_CPA ? 0 : e2max) * 4 + 16 +
+         (EIK_CPA ? (size_t)e1max * 64 + (size_t)TILE * 32 + (size_t)2 * e2_round4(e2max) * 4 + 16
+                  : 0);
 }
 
 // single-role pass: one tile buffer after a 128-byte header
@@ -434,24 +482,48 @@ __device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TileSmem t;
   t.cb = nullptr;
-  double2* q = reinterpret_cast<double2*>(dsm + 128);
+  t.vmb = reinterpret_cast<double4*>(dsm + 128);
+  double2* q = reinterpret_cast<double2*>(dsm + 128 + (EIK_VMB ? TILE * 32 : 0));
   t.x = SArr{q, S.e2max};
   q += 2 * S.e2max;
   t.La = SArr{q, S.e1max};
   q += 2 * S.e1max;
   t.U = SArr{q, S.e1max};
   q += 2 * S.e1max;
+#if EIK_CPA
+  unsigned char* p = reinterpret_cast<unsigned char*>(q);
+  t.neb = reinterpret_cast<double4*>(p);
+  p += (size_t)TILE * 32;
+  t.lce1 = reinterpret_cast<double*>(p);
+  p += (size_t)S.e1max * 48;
+  t.rows = reinterpret_cast<short*>(p);
+  p += (size_t)S.e1max * 16;
+  t.map0 = reinterpret_cast<int*>(p);
+  t.map1 = t.map0 + e2_round4(S.e2max);
+  p += (size_t)2 * e2_round4(S.e2max) * 4;
+  t.gid = reinterpret_cast<int*>(p);
+#else
   t.gid = reinterpret_cast<int*>(q);
+#endif
   return t;
 }
 
 __host__ __device__ constexpr size_t tw_buf_bytes(int e1max, int e2max) {
   return ((size_t)e2max * 32 + (size_t)e1max * 64 + 127) / 128 * 128;
 }
+// SR2 layout (after a 128-byte mbarrier header), every part 16-byte aligned:
+// cb [NCOEF][TILE] | neb [TILE] | vmb [TILE] | rows [e1][8] short |
+// lce1 [e1][6] | map [2][e2r] int | x [e2] | La [e1] | U [e1]   (SArr halves)
+__host__ __device__ constexpr int sr2_e2r(int e2max) { return (e2max + 3) & ~3; }
+__host__ __device__ constexpr size_t sr2_smem_bytes(int e1max, int e2max) {
+  return 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 64 + (size_t)e1max * 16 +
+         (size_t)e1max * 48 + (size_t)2 * sr2_e2r(e2max) * 4 + (size_t)e2max * 32 +
+         (size_t)e1max * 64;
+}
 __host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
   return WS == 2 ? 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
                        2 * tw_buf_bytes(e1max, e2max)
-                 : 128 + tile_buf_bytes(e1max, e2max);
+                 : (SR2 ? sr2_smem_bytes(e1max, e2max) : 128 + tile_buf_bytes(e1max, e2max));
 }
 
 // ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
@@ -505,6 +577,20 @@ __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// per-thread asynchronous 16-byte global -> shared copies (LDGSTS)
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void pf_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// L2 prefetch of tile t's own-cell coefficient runs and E1 Laplacian rows,
+// spread over the CTA's threads (128-byte lines)
+__device__ __forceinline__ void tile_prefetch_l2(const SweOp& S, int t);
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 struct Row8 {
   short s[8];
 };
@@ -524,6 +610,77 @@ struct JvAcc {
 #ifndef EIK_CHUNK
 #define EIK_CHUNK 3
 #endif
+// One chunk of CH slots' G/D/V coefficients of own cell i (9 per slot).
+template <int CH>
+struct CoefChunk {
+  double v[CH][9];
+};
+template <int CH>
+__device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, CoefChunk<CH>& cf) {
+  const int64_t st = (int64_t)9 * S.NC;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const double* cp = S.coefc + i + (s0 + k) * st;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) cf.v[k][q] = __ldcs(cp + q * S.NC);
+  }
+}
+template <int CH>
+__device__ __forceinline__ void coef_load_smem(const TileSmem& ts, int c, int s0,
+                                               CoefChunk<CH>& cf) {
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const double* cp = ts.cb + ((s0 + k) * 9) * TILE + c;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) cf.v[k][q] = cp[q * TILE];
+  }
+}
+// own-cell terms shared by every slot
+struct JvOwn {
+  double4 ai, Ui, lai;
+  double ei, fxi, fyi, fzi;
+};
+__device__ __forceinline__ JvOwn jv_own(const SweOp& S, double4 ai, double4 Ui, double4 lai) {
+  JvOwn o;
+  o.ai = ai;
+  o.Ui = Ui;
+  o.lai = lai;
+  o.ei = Ui.x * ai.x + Ui.y * ai.y + Ui.z * ai.z + S.g * ai.w;
+  o.fxi = Ui.w * ai.x + Ui.x * ai.w;
+  o.fyi = Ui.w * ai.y + Ui.y * ai.w;
+  o.fzi = Ui.w * ai.z + Ui.z * ai.w;
+  return o;
+}
+// accumulate slots [s0, s0+CH) with their coefficients in cf
+template <int CH>
+__device__ __forceinline__ void jv_accum(const SweOp& S, const TileSmem& ts, const short* row,
+                                         const double* lc, int s0, const CoefChunk<CH>& cf,
+                                         const JvOwn& o, JvAcc& a) {
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int s = s0 + k;
+    const int l = row[s];
+    const double vx = cf.v[k][0], vy = cf.v[k][1], vz = cf.v[k][2];
+    const double gcx = cf.v[k][3], gcy = cf.v[k][4], gcz = cf.v[k][5];
+    const double dx = cf.v[k][6], dy = cf.v[k][7], dz = cf.v[k][8];
+    const double l0 = lc[s];
+    const double4 aj = sld(ts.x, l);
+    const double4 U = sld(ts.U, l);
+    const double4 la = sld(ts.La, l);
+    a.zeta += vx * (aj.x - o.ai.x) + vy * (aj.y - o.ai.y) + vz * (aj.z - o.ai.z);
+    const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
+    a.gx += gcx * (e - o.ei);
+    a.gy += gcy * (e - o.ei);
+    a.gz += gcz * (e - o.ei);
+    a.dv += dx * ((U.w * aj.x + U.x * aj.w) + o.fxi) + dy * ((U.w * aj.y + U.y * aj.w) + o.fyi) +
+            dz * ((U.w * aj.z + U.z * aj.w) + o.fzi);
+    a.l0 += l0 * (la.x - o.lai.x);
+    a.l1 += l0 * (la.y - o.lai.y);
+    a.l2 += l0 * (la.z - o.lai.z);
+    a.l3 += l0 * (la.w - o.lai.w);
+  }
+}
+
 // Slots are processed in chunks of EIK_CHUNK: all 9*CHUNK coefficient loads
 // of a chunk are issued before any of them is used (a compiler memory fence
 // keeps them together), so each thread keeps ~27 streaming loads in flight
@@ -533,52 +690,16 @@ __device__ __forceinline__ JvAcc swe_jv_part(const SweOp& S, const TileSmem& ts,
                                              const double* lc, int s0, int c, int64_t i,
                                              double4 ai, double4 Ui, double4 lai) {
   // kSrc: 0 = coefficients from global, 1 = from the TMA-staged smem block
-  const double ei = Ui.x * ai.x + Ui.y * ai.y + Ui.z * ai.z + S.g * ai.w;
-  const double fxi = Ui.w * ai.x + Ui.x * ai.w, fyi = Ui.w * ai.y + Ui.y * ai.w,
-               fzi = Ui.w * ai.z + Ui.z * ai.w;
+  const JvOwn o = jv_own(S, ai, Ui, lai);
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t st = (int64_t)9 * S.N;
   constexpr int CH = (EIK_CHUNK < NS) ? EIK_CHUNK : NS;
 #pragma unroll
   for (int k0 = 0; k0 < NS; k0 += CH) {
-    double cf[CH][9];
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const int s = s0 + k0 + k;
-      if constexpr (kSrc == 1) {
-        const double* cp = ts.cb + (s * 9) * TILE + c;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) cf[k][q] = cp[q * TILE];
-      } else {
-        const double* cp = S.coefc + i + s * st;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) cf[k][q] = __ldcs(cp + q * S.N);
-      }
-    }
+    CoefChunk<CH> cf;
+    if constexpr (kSrc == 1) coef_load_smem<CH>(ts, c, s0 + k0, cf);
+    else coef_load<CH>(S, i, s0 + k0, cf);
     if constexpr (kSrc == 0) asm volatile("" ::: "memory");
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const int s = s0 + k0 + k;
-      const int l = row[s];
-      const double vx = cf[k][0], vy = cf[k][1], vz = cf[k][2];
-      const double gcx = cf[k][3], gcy = cf[k][4], gcz = cf[k][5];
-      const double dx = cf[k][6], dy = cf[k][7], dz = cf[k][8];
-      const double l0 = lc[s];
-      const double4 aj = sld(ts.x, l);
-      const double4 U = sld(ts.U, l);
-      const double4 la = sld(ts.La, l);
-      a.zeta += vx * (aj.x - ai.x) + vy * (aj.y - ai.y) + vz * (aj.z - ai.z);
-      const double e = U.x * aj.x + U.y * aj.y + U.z * aj.z + S.g * aj.w;
-      a.gx += gcx * (e - ei);
-      a.gy += gcy * (e - ei);
-      a.gz += gcz * (e - ei);
-      a.dv += dx * ((U.w * aj.x + U.x * aj.w) + fxi) + dy * ((U.w * aj.y + U.y * aj.w) + fyi) +
-              dz * ((U.w * aj.z + U.z * aj.w) + fzi);
-      a.l0 += l0 * (la.x - lai.x);
-      a.l1 += l0 * (la.y - lai.y);
-      a.l2 += l0 * (la.z - lai.z);
-      a.l3 += l0 * (la.w - lai.w);
-    }
+    jv_accum<CH>(S, ts, row, lc, s0 + k0, cf, o, a);
   }
   return a;
 }
@@ -726,7 +847,7 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
           mbar_expect_tx(t0.cfull + h, bytes);
           if (nT > 0) {
             for (int q = h * HALF_RUNS; q < (h + 1) * HALF_RUNS; ++q)
-              tma_g2s_ef(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.N + c0, run,
+              tma_g2s_ef(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.NC + c0, run,
                          t0.cfull + h, pol);
             if (h == NST - 1) tma_g2s(t0.neb, S.ne + c0, nT * 32u, t0.cfull + h);
           }
@@ -903,27 +1024,104 @@ __device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi&
 #undef TWP_END
 }
 
-// Single-role tiled pass (the default): every thread does the
-// three steps of a tile in turn, separated by __syncthreads.
+// ---- SR2: single-role pass with TMA-staged per-tile static data ----------
+struct Sr2Smem {
+  unsigned long long* mb;  // [0..1] map buffers, [2] small statics, [3] coefficients
+  double* cb;              // [NCOEF][TILE]
+  double4* neb;            // [TILE] (n, eta) of the own cells
+  double4* vmb;            // [TILE] own-cell vector handed to the epilogue
+  short* rows;             // [e1max][8]
+  double* lce1;            // [e1max][6]
+  int* map[2];             // [e2r]
+  SArr x, La, U;
+};
+__device__ __forceinline__ Sr2Smem sr2_smem(const SweOp& S) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Sr2Smem t;
+  unsigned char* p = dsm;
+  t.mb = reinterpret_cast<unsigned long long*>(p);
+  p += 128;
+  t.cb = reinterpret_cast<double*>(p);
+  p += (size_t)NCOEF * TILE * 8;
+  t.neb = reinterpret_cast<double4*>(p);
+  p += (size_t)TILE * 32;
+  t.vmb = reinterpret_cast<double4*>(p);
+  p += (size_t)TILE * 32;
+  t.rows = reinterpret_cast<short*>(p);
+  p += (size_t)S.e1max * 16;
+  t.lce1 = reinterpret_cast<double*>(p);
+  p += (size_t)S.e1max * 48;
+  const int e2r = sr2_e2r(S.e2max);
+  t.map[0] = reinterpret_cast<int*>(p);
+  t.map[1] = t.map[0] + e2r;
+  p += (size_t)2 * e2r * 4;
+  double2* q = reinterpret_cast<double2*>(p);
+  t.x = SArr{q, S.e2max};
+  q += 2 * S.e2max;
+  t.La = SArr{q, S.e1max};
+  q += 2 * S.e1max;
+  t.U = SArr{q, S.e1max};
+  return t;
+}
+
 template <class Epi>
-__device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
-  if constexpr (WS == 2) {
-    swe_tiled_tw(sm, S, F, epi);
-    return;
+__device__ void swe_tiled_sr2(const SweOp& S, const Form& F, const Epi& epi) {
+  const Sr2Smem L = sr2_smem(S);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(L.mb + q, 1);
   }
-  const TileSmem ts = tile_smem(S);
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+  __syncthreads();
+  // one thread issues every bulk copy of a tile; the cell map of the next
+  // tile goes one tile ahead (double-buffered) so the halo gather of a tile
+  // starts without a dependent global round trip
+  auto issue_map = [&](int t, int b) {
+    const uint32_t bytes = ((uint32_t)__ldg(S.t_nE2 + t) * 4u + 15u) & ~15u;
+    mbar_expect_tx(L.mb + b, bytes);
+    if (bytes) tma_g2s(b ? L.map[1] : L.map[0], S.e2map + __ldg(S.t_e2off + t), bytes, L.mb + b);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < S.ntiles) {
+    fence_proxy_async_shared();
+    issue_map(blockIdx.x, 0);
+  }
+  uint32_t ph_map = 0u, ph_s = 0u, ph_c = 0u;  // mbarrier parities (map: one bit per buffer)
+  int k = 0;
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x, ++k) {
+    const int b = k & 1;
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-    if (nT == 0) continue;  // uniform over the CTA
-    const int* map = S.e2map + __ldg(S.t_e2off + t);
-    const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+    const int e1off = __ldg(S.t_e1off + t);
+    if (threadIdx.x == 0) {
+      // every thread finished the previous tile (barrier at its end): the
+      // generic-proxy reads of these buffers are ordered before the copies
+      fence_proxy_async_shared();
+      const uint32_t rb = (uint32_t)nE1 * 16u, lb = (uint32_t)nE1 * 48u, nb = (uint32_t)nT * 32u;
+      mbar_expect_tx(L.mb + 2, rb + lb + nb);
+      if (nE1) {
+        tma_g2s(L.rows, S.lnbr + (int64_t)e1off * 8, rb, L.mb + 2);
+        tma_g2s(L.lce1, S.LcE1 + (int64_t)e1off * 6, lb, L.mb + 2);
+      }
+      if (nT) tma_g2s(L.neb, S.ne + c0, nb, L.mb + 2);
+      // runs rounded up to 16 bytes (odd last tile): the extra element is the
+      // next run's first (or the allocation's slack), never read
+      const uint32_t run = ((uint32_t)nT * 8u + 15u) & ~15u;
+      mbar_expect_tx(L.mb + 3, run * NCOEF);
+      if (nT) {
+        const uint64_t pol = l2_evict_first_policy();
+        for (int q = 0; q < NCOEF; ++q)
+          tma_g2s_ef(L.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.NC + c0, run, L.mb + 3,
+                     pol);
+      }
+      if (t + (int)gridDim.x < S.ntiles) issue_map(t + gridDim.x, b ^ 1);
+    }
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
+    mbar_wait(L.mb + b, (ph_map >> b) & 1u);
+    ph_map ^= 1u << b;
+    const int* map = b ? L.map[1] : L.map[0];
     for (int base = 0; base < nE2; base += 2 * TPB) {
       const int ca = base + threadIdx.x, cb = ca + TPB;
       const bool va = ca < nE2, vb = cb < nE2;
-      const int ga = va ? __ldg(map + ca) : 0;
-      const int gb = vb ? __ldg(map + cb) : 0;
+      const int ga = va ? map[ca] : 0;
+      const int gb = vb ? map[cb] : 0;
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
               b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
       if (va) {
@@ -940,27 +1138,250 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       }
       if (va) {
         const double4 x = form_x(F, a0, a1, a2);
-        ts.gid[ca] = ga;
-        sst(ts.x, ca, x);
-        if (ca < nE1) sst(ts.U, ca, ua);
-        if (F.out && ca < nT) stv(F.out + ga, x);
+        sst(L.x, ca, x);
+        if (ca < nE1) sst(L.U, ca, ua);
+        if (ca < nT) {
+          if (F.out) stv(F.out + ga, x);
+          if (F.epi_vm1) L.vmb[ca] = (F.epi_vm1 == F.vm1) ? a2 : ldv(F.epi_vm1 + ga);
+        }
       }
       if (vb) {
         const double4 x = form_x(F, b0, b1, b2);
-        ts.gid[cb] = gb;
-        sst(ts.x, cb, x);
-        if (cb < nE1) sst(ts.U, cb, ub);
-        if (F.out && cb < nT) stv(F.out + gb, x);
+        sst(L.x, cb, x);
+        if (cb < nE1) sst(L.U, cb, ub);
+        if (cb < nT) {
+          if (F.out) stv(F.out + gb, x);
+          if (F.epi_vm1) L.vmb[cb] = (F.epi_vm1 == F.vm1) ? b2 : ldv(F.epi_vm1 + gb);
+        }
       }
     }
     __syncthreads();
-    // step 2: L x on E1 (difference form)
+    // step 2: L x on E1 (difference form), rows and coefficients in smem
+    mbar_wait(L.mb + 2, ph_s);
+    ph_s ^= 1u;
     for (int c = threadIdx.x; c < nE1; c += TPB) {
+      const Row8 row = *reinterpret_cast<const Row8*>(L.rows + c * 8);
+      const double2* lc2 = reinterpret_cast<const double2*>(L.lce1 + c * 6);
+      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
+      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
+      const double4 xc = sld(L.x, c);
+      double4 acc = d4(0.0);
+#pragma unroll
+      for (int s2 = 0; s2 < KCMAX; ++s2) {
+        const double l = lv[s2];
+        const double4 xv = sld(L.x, row.s[s2]);
+        acc.x += l * (xv.x - xc.x);
+        acc.y += l * (xv.y - xc.y);
+        acc.z += l * (xv.z - xc.z);
+        acc.w += l * (xv.w - xc.w);
+      }
+      sst(L.La, c, acc);
+    }
+    __syncthreads();
+    // step 3: z = scale * J x on the own cells, SR2_TPC threads per cell
+    mbar_wait(L.mb + 3, ph_c);
+    ph_c ^= 1u;
+    {
+      constexpr int NSL = KCMAX / SR2_TPC;
+      const int c = threadIdx.x / SR2_TPC;
+      const int part = threadIdx.x % SR2_TPC;
+      {
+        const bool live = c < nT;
+        const int cc = live ? c : 0;
+        const int64_t i = c0 + cc;
+        // (row and Laplacian coefficients read from shared memory: the slot
+        // range depends on `part`, register arrays would go to local memory)
+        const short* row = L.rows + cc * 8;
+        const double* lcr = L.lce1 + cc * 6;
+        const double4 ai = sld(L.x, cc);
+        const double4 Ui = sld(L.U, cc);
+        const double4 lai = sld(L.La, cc);
+        TileSmem ts;
+        ts.cb = L.cb;
+        ts.x = L.x;
+        ts.La = L.La;
+        ts.U = L.U;
+        ts.gid = nullptr;
+        JvAcc a = swe_jv_part<1, NSL>(S, ts, row, lcr, part * NSL, cc, i, ai, Ui, lai);
+#pragma unroll
+        for (int o = 1; o < SR2_TPC; o <<= 1) {
+          a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, o);
+          a.gx += __shfl_xor_sync(0xffffffffu, a.gx, o);
+          a.gy += __shfl_xor_sync(0xffffffffu, a.gy, o);
+          a.gz += __shfl_xor_sync(0xffffffffu, a.gz, o);
+          a.dv += __shfl_xor_sync(0xffffffffu, a.dv, o);
+          a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, o);
+          a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, o);
+          a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, o);
+          a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, o);
+        }
+        if (live && part == 0) {
+          const double4 z = S.scale * swe_jv_finish(S, a, L.neb[cc], ai, Ui);
+          const double4 vm = F.epi_vm1 ? L.vmb[cc] : d4(0.0);
+          epi(i, z, ai, vm);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Single-role tiled pass (the default): every thread does the
+// three steps of a tile in turn, separated by __syncthreads.
+template <class Epi>
+__device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
+  if constexpr (WS == 2) {
+    swe_tiled_tw(sm, S, F, epi);
+    return;
+  }
+  if constexpr (SR2 != 0) {
+    swe_tiled_sr2(S, F, epi);
+    return;
+  }
+  const TileSmem ts = tile_smem(S);
+#if EIK_PROF
+  long long pst[3] = {0, 0, 0}, pt = clock64();
+#define SRP_MARK(k) { const long long n_ = clock64(); pst[k] += n_ - pt; pt = n_; }
+#else
+#define SRP_MARK(k)
+#endif
+#if EIK_CPA
+  // Every tile's contiguous static data (local neighbour rows and Laplacian
+  // rows of E1, (n, eta) of the own cells) is copied to shared memory by
+  // cp.async while the halo is gathered; the cell map of the next tile is
+  // copied one tile ahead, so the gather starts without a dependent global
+  // round trip.
+  auto issue_map = [&](int t, int* dst) {
+    const int n4 = (__ldg(S.t_nE2 + t) + 3) >> 2;
+    const int* src = S.e2map + __ldg(S.t_e2off + t);
+    for (int q = threadIdx.x; q < n4; q += TPB) cp16(dst + 4 * q, src + 4 * q);
+  };
+  if ((int)blockIdx.x < S.ntiles) {
+    issue_map(blockIdx.x, ts.map0);
+    cp_commit();
+    cp_wait_all();
+  }
+  __syncthreads();
+  int kt = 0;
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x, ++kt) {
+    const int64_t c0 = __ldg(S.t_cell0 + t);
+    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+    const int e1off = __ldg(S.t_e1off + t);
+    {
+      const short* rg = S.lnbr + (int64_t)e1off * 8;
+      const double* lg = S.LcE1 + (int64_t)e1off * 6;
+      for (int q = threadIdx.x; q < nE1; q += TPB) {
+        cp16(ts.rows + q * 8, rg + q * 8);
+        cp16(ts.lce1 + q * 6, lg + q * 6);
+        cp16(ts.lce1 + q * 6 + 2, lg + q * 6 + 2);
+        cp16(ts.lce1 + q * 6 + 4, lg + q * 6 + 4);
+      }
+      for (int q = threadIdx.x; q < 2 * nT; q += TPB)
+        cp16(reinterpret_cast<double*>(ts.neb) + 2 * q,
+             reinterpret_cast<const double*>(S.ne + c0) + 2 * q);
+      if (t + (int)gridDim.x < S.ntiles) issue_map(t + gridDim.x, (kt & 1) ? ts.map0 : ts.map1);
+      cp_commit();
+    }
+    if (nT == 0) {  // uniform over the CTA
+      cp_wait_all();
+      __syncthreads();
+      continue;
+    }
+    const int* map = (kt & 1) ? ts.map1 : ts.map0;
+    const short* rows = ts.rows;
+#else
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+    const int64_t c0 = __ldg(S.t_cell0 + t);
+    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
+    if (nT == 0) continue;  // uniform over the CTA
+    const int* map = S.e2map + __ldg(S.t_e2off + t);
+    const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
+#endif
+#if EIK_L2PF == 1
+    tile_prefetch_l2(S, t);
+#elif EIK_L2PF == 2
+    if (t == (int)blockIdx.x) tile_prefetch_l2(S, t);
+    if (t + (int)gridDim.x < S.ntiles) tile_prefetch_l2(S, t + gridDim.x);
+#endif
+    // step 1: x on E2 (two cells per thread per round, all loads issued first)
+    for (int base = 0; base < nE2; base += 2 * TPB) {
+      const int ca = base + threadIdx.x, cb = ca + TPB;
+      const bool va = ca < nE2, vb = cb < nE2;
+#if EIK_CPA
+      const int ga = va ? map[ca] : 0;
+      const int gb = vb ? map[cb] : 0;
+#else
+      const int ga = va ? __ldg(map + ca) : 0;
+      const int gb = vb ? __ldg(map + cb) : 0;
+#endif
+      double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
+              b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
+      if (va) {
+        a0 = ldv(F.src + ga);
+        if (F.vm2) a1 = ldv(F.vm2 + ga);
+        if (F.vm1) a2 = ldv(F.vm1 + ga);
+        if (ca < nE1) ua = ldv_nc(S.lin + ga);
+      }
+      if (vb) {
+        b0 = ldv(F.src + gb);
+        if (F.vm2) b1 = ldv(F.vm2 + gb);
+        if (F.vm1) b2 = ldv(F.vm1 + gb);
+        if (cb < nE1) ub = ldv_nc(S.lin + gb);
+      }
+      if (va) {
+        const double4 x = form_x(F, a0, a1, a2);
+        if (!EIK_LCE1) ts.gid[ca] = ga;
+        sst(ts.x, ca, x);
+        if (ca < nE1) sst(ts.U, ca, ua);
+        if (F.out && ca < nT) stv(F.out + ga, x);
+#if EIK_VMB
+        if (F.epi_vm1 && ca < nT) ts.vmb[ca] = (F.epi_vm1 == F.vm1) ? a2 : ldv(F.epi_vm1 + ga);
+#endif
+      }
+      if (vb) {
+        const double4 x = form_x(F, b0, b1, b2);
+        if (!EIK_LCE1) ts.gid[cb] = gb;
+        sst(ts.x, cb, x);
+        if (cb < nE1) sst(ts.U, cb, ub);
+        if (F.out && cb < nT) stv(F.out + gb, x);
+#if EIK_VMB
+        if (F.epi_vm1 && cb < nT) ts.vmb[cb] = (F.epi_vm1 == F.vm1) ? b2 : ldv(F.epi_vm1 + gb);
+#endif
+      }
+    }
+#if EIK_CPA
+    cp_wait_all();
+#endif
+    __syncthreads();
+    SRP_MARK(0)
+#if EIK_PRE3
+    // step 3's first coefficient chunk goes out now, in flight during step 2
+    constexpr int PCH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
+    CoefChunk<PCH> pre;
+    if ((int)threadIdx.x < nT) coef_load<PCH>(S, c0 + threadIdx.x, 0, pre);
+#endif
+    // step 2: L x on E1 (difference form)
+    const double* lce1 = S.LcE1 + (int64_t)__ldg(S.t_e1off + t) * 6;
+    for (int c = threadIdx.x; c < nE1; c += TPB) {
+#if EIK_CPA
+      const Row8 row = *reinterpret_cast<const Row8*>(rows + c * 8);
+#else
       const Row8 row = load_row8(rows + (int64_t)c * 8);
+#endif
+#if EIK_CPA
+      const double2* lc2 = reinterpret_cast<const double2*>(ts.lce1 + c * 6);
+      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
+      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
+#elif EIK_LCE1
+      const double2 l01 = ldv2_nc(lce1 + (int64_t)c * 6), l23 = ldv2_nc(lce1 + (int64_t)c * 6 + 2),
+                    l45 = ldv2_nc(lce1 + (int64_t)c * 6 + 4);
+      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
+#else
       const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
       const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(lc));
       const double2 l45 = ldv2_nc(lc + 4);
       const double lv[6] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y};
+#endif
       const double4 xc = sld(ts.x, c);
       double4 acc = d4(0.0);
 #pragma unroll
@@ -975,6 +1396,7 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       sst(ts.La, c, acc);
     }
     __syncthreads();
+    SRP_MARK(1)
     // step 3: z = scale * J x on the own cells
     if ((int)threadIdx.x < nT) {
       const int c = threadIdx.x;
@@ -982,17 +1404,95 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       const double4 ai = sld(ts.x, c);
       const double4 Ui = sld(ts.U, c);
       const double4 lai = sld(ts.La, c);
+#if EIK_CPA
+      const Row8 row = *reinterpret_cast<const Row8*>(rows + c * 8);
+      const double2* lc2 = reinterpret_cast<const double2*>(ts.lce1 + c * 6);
+      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
+      const double lcr[8] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y, 0.0, 0.0};
+#elif EIK_LCE1
+      const Row8 row = load_row8(rows + (int64_t)c * 8);
+      const double2 l01 = ldv2_nc(lce1 + (int64_t)c * 6), l23 = ldv2_nc(lce1 + (int64_t)c * 6 + 2),
+                    l45 = ldv2_nc(lce1 + (int64_t)c * 6 + 4);
+      const double lcr[8] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y, 0.0, 0.0};
+#else
       const Row8 row = load_row8(rows + (int64_t)c * 8);
       const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(S.Lc + i * 8));
       const double2 l45 = ldv2_nc(S.Lc + i * 8 + 4);
       const double lcr[8] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y, 0.0, 0.0};
+#endif
+#if EIK_PRE3
+      const JvOwn o = jv_own(S, ai, Ui, lai);
+      JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      jv_accum<PCH>(S, ts, row.s, lcr, 0, pre, o, a);
+#pragma unroll
+      for (int k0 = PCH; k0 < KCMAX; k0 += PCH) {
+        CoefChunk<PCH> cf;
+        coef_load<PCH>(S, i, k0, cf);
+        asm volatile("" ::: "memory");
+        jv_accum<PCH>(S, ts, row.s, lcr, k0, cf, o, a);
+      }
+#elif EIK_PIPE3
+      // software-pipelined coefficient stream: chunk k+1's loads are issued
+      // before chunk k's math, so a thread always has a chunk in flight
+      constexpr int PC = EIK_PIPE3;
+      const JvOwn o = jv_own(S, ai, Ui, lai);
+      JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      CoefChunk<PC> cA, cB;
+      coef_load<PC>(S, i, 0, cA);
+#pragma unroll
+      for (int k0 = 0; k0 < KCMAX; k0 += 2 * PC) {
+        if (k0 + PC < KCMAX) coef_load<PC>(S, i, k0 + PC, cB);
+        asm volatile("" ::: "memory");
+        jv_accum<PC>(S, ts, row.s, lcr, k0, cA, o, a);
+        if (k0 + PC < KCMAX) {
+          if (k0 + 2 * PC < KCMAX) coef_load<PC>(S, i, k0 + 2 * PC, cA);
+          asm volatile("" ::: "memory");
+          jv_accum<PC>(S, ts, row.s, lcr, k0 + PC, cB, o, a);
+        }
+      }
+#else
       const JvAcc a = swe_jv_part<0, KCMAX>(S, ts, row.s, lcr, 0, c, i, ai, Ui, lai);
+#endif
+#if EIK_CPA
+      const double4 z = S.scale * swe_jv_finish(S, a, ts.neb[c], ai, Ui);
+#else
       const double4 z = S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
+#endif
+#if EIK_VMB
+      const double4 vm = F.epi_vm1 ? ts.vmb[c] : d4(0.0);
+#else
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
+#endif
       epi(i, z, ai, vm);
     }
     __syncthreads();
+    SRP_MARK(2)
   }
+#if EIK_PROF
+  if (S.prof && threadIdx.x == 0) {
+    for (int k = 0; k < 3; ++k) atomicAdd(S.prof + k, (unsigned long long)pst[k]);
+    atomicAdd(S.prof + 3, 1ull);
+  }
+#endif
+#undef SRP_MARK
+}
+
+__device__ __forceinline__ void tile_prefetch_l2(const SweOp& S, int t) {
+  const int64_t c0 = __ldg(S.t_cell0 + t);
+  const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t);
+  if (nT <= 0) return;
+  const char* base0 = reinterpret_cast<const char*>(S.coefc + c0);
+  const int64_t lo = (int64_t)(reinterpret_cast<uintptr_t>(base0) & 127);
+  const int lines = (int)((lo + (int64_t)nT * 8 + 127) >> 7);
+  const char* aligned = base0 - lo;
+  const int tot = NCOEF * lines;
+  for (int q = threadIdx.x; q < tot; q += TPB) {
+    const int r = q / lines, l = q - r * lines;
+    pf_l2(aligned + (int64_t)r * S.NC * 8 + (int64_t)l * 128);
+  }
+  const char* lb = reinterpret_cast<const char*>(S.LcE1 + (int64_t)__ldg(S.t_e1off + t) * 6);
+  const int ll = (nE1 * 48 + 127) >> 7;
+  for (int q = threadIdx.x; q < ll; q += TPB) pf_l2(lb + (int64_t)q * 128);
 }
 
 struct SrcPtr {

@@ -144,6 +144,19 @@ class SweContext:
     def last_kernel_ms(self):
         return float(nat.load().eik_swe_last_kernel_ms(self.h))
 
+    def set_hostloop(self, on=True):
+        """Launch the split step kernel by kernel (no CUDA graph): every
+        Krylov sweep is timed with CUDA events and ncu can profile it."""
+        nat.check(nat.load().eik_swe_set_hostloop(self.h, 1 if on else 0), "set_hostloop")
+
+    def sweep_timing(self, reset=False):
+        """(ms, sweeps) of the Krylov sweep kernels run in host-loop mode."""
+        ms = C.c_double(0.0)
+        n = C.c_int64(0)
+        nat.check(nat.load().eik_swe_sweep_timing(self.h, C.byref(ms), C.byref(n),
+                                                  1 if reset else 0), "sweep_timing")
+        return float(ms.value), int(n.value)
+
 
 _CTX = {}
 

@@ -42,11 +42,14 @@ print(json.dumps(out))
 """
 
 
-def _run(mono):
+def _run(mono, host=False):
     env = dict(os.environ)
     env.pop("EIK_STEP_MONO", None)
+    env.pop("EIK_STEP_HOST", None)
     if mono:
         env["EIK_STEP_MONO"] = "1"
+    if host:
+        env["EIK_STEP_HOST"] = "1"
     r = subprocess.run([sys.executable, "-c", _SCRIPT % ROOT], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -66,3 +69,12 @@ def test_split_step_matches_monolithic_bitwise():
         nsteps = len(split[k]["calls"])
         assert mono[k]["launches"] >= nsteps
         assert split[k]["launches"] >= mono[k]["launches"] + 2 * nsteps
+
+
+def test_hostloop_matches_graph_bitwise():
+    """Host-loop mode (kernel-by-kernel launches, used for the sweep roofline
+    and ncu) runs exactly the graph's kernels: same bits, same counters."""
+    graph, host = _run(False), _run(False, host=True)
+    for k in graph:
+        assert graph[k]["calls"] == host[k]["calls"], k
+        assert graph[k]["u"] == host[k]["u"], k

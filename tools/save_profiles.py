@@ -29,6 +29,7 @@ if os.path.exists(p):
         for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             fh.write(f"{name:24s} launches={n:4d} total_ns={t:14.0f} share={100 * t / tot:6.2f}%\n")
 rep = os.path.join(src, f"step_{tag}.ncu-rep")
+kskip = int(os.environ.get("KSKIP", "4"))
 if os.path.exists(rep):
     out = subprocess.run([sys.executable, "tools/ncu_summary.py", rep], capture_output=True, text=True).stdout
     r = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True)
@@ -38,7 +39,31 @@ if os.path.exists(rep):
     det = [f"{r[si][:30]:30s} {r[mi]:48s} {r[vi]:>16s} {r[ui]}" for r in rows[1:]
            if r[si] in ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Occupancy",
                         "Launch Statistics", "Warp State Statistics", "Compute Workload Analysis")]
-    with open(os.path.join(dst, f"ncu_full_k_swe_step_{tag}.txt"), "w") as fh:
-        fh.write(f"ncu --set full --clock-control none -k regex:k_swe_step -s 1 -c 1 "
-                 f"(one C3 L8 exprb42 step)\n\n{out}\n\n" + "\n".join(det) + "\n")
+    # Krylov iterations of the captured launch (EIK_SWEEP_LOG lines of the ncu run)
+    iters = None
+    logp = os.path.join(src, f"ncu_full_{tag}.log")
+    if os.path.exists(logp):
+        for line in open(logp):
+            if line.startswith(f"[eik] sweep {kskip} iters "):
+                iters = int(line.split()[4])
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True)
+    rr = list(csv.reader(io.StringIO(raw.stdout)))
+    h, u, v = rr[0], rr[1], rr[2]
+
+    def metric(name):
+        x = float(v[h.index(name)].replace(",", ""))
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
+        return x * scale.get(u[h.index(name)], 1.0)
+    dram = metric("dram__bytes_read.sum") + metric("dram__bytes_write.sum")
+    with open(os.path.join(dst, f"ncu_full_k_swe_sweep_{tag}.txt"), "w") as fh:
+        fh.write(f"ncu --set full --clock-control none -k regex:k_swe_sweep -s {kskip} -c 1 "
+                 f"(one Krylov sweep launch of a C3 L8 exprb42 step, host-loop mode; "
+                 f"{iters} Krylov iterations in the launch; DRAM bytes per iteration "
+                 f"{dram / iters / 1e6 if iters else float('nan'):.1f} MB)\n\n{out}\n\n"
+                 + "\n".join(det) + "\n")
+    if iters:
+        json.dump({"source": f"profiles/ncu_full_k_swe_sweep_{tag}.txt", "kernel": "k_swe_sweep",
+                   "cells": 655362, "dram_bytes_per_launch": dram, "krylov_iters_in_launch": iters,
+                   "dram_bytes_per_iter": dram / iters},
+                  open(os.path.join(dst, "traffic.json"), "w"), indent=1)
 print(sorted(os.listdir(dst)))
