@@ -47,19 +47,26 @@ __device__ __forceinline__ void smem_init(Smem& sm) {
 }
 
 // (u_x; u_y; u_z; h) SoA  <->  per-cell double4
-__global__ void k_soa_to_cell(const double* __restrict__ s, double4* d, int64_t N) {
+// (user cell order, see the device cell order in eik_swe_create: device cell
+// i is user cell ord[i])
+__global__ void k_soa_to_cell(const double* __restrict__ s, double4* d, int64_t N,
+                              const int* __restrict__ ord) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    d[i] = make_double4(s[i], s[N + i], s[2 * N + i], s[3 * N + i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = ord[i];
+    d[i] = make_double4(s[u], s[N + u], s[2 * N + u], s[3 * N + u]);
+  }
 }
-__global__ void k_cell_to_soa(const double4* __restrict__ d, double* s, int64_t N) {
+__global__ void k_cell_to_soa(const double4* __restrict__ d, double* s, int64_t N,
+                              const int* __restrict__ ord) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double4 v = d[i];
-    s[i] = v.x;
-    s[N + i] = v.y;
-    s[2 * N + i] = v.z;
-    s[3 * N + i] = v.w;
+    const int64_t u = ord[i];
+    s[u] = v.x;
+    s[N + u] = v.y;
+    s[2 * N + u] = v.z;
+    s[3 * N + u] = v.w;
   }
 }
 
@@ -119,7 +126,6 @@ __device__ int phase_rhs(cg::grid_group& grid, Smem& sm, const SweOp& S,
     if (out_v) out_v[i] = dt * F;
     r[0] += nf4(F) + nf4(w[i]);
   }
-  if (write_eta) fence_proxy_async_global();  // ne is read by TMA later
   grid_reduce<1>(grid, sm, r, part);
   return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
 }
@@ -702,6 +708,43 @@ int coop_grid(const void* const* kernels, int nk, int dev, int64_t NU, size_t sm
   return (int)std::max<int64_t>(1, std::min<int64_t>(best, need));
 }
 
+// Recursive coordinate bisection of ord[lo, hi) into nt leaves of sizes
+// differing by at most one; leaf starts are appended to `starts` in order.
+// Each leaf is left sorted by user index (the grid's own locality order).
+void rcb_order(const double* px, const double* py, const double* pz, int32_t* ord, int64_t lo,
+               int64_t hi, int nt, std::vector<int32_t>& starts) {
+  const int64_t n = hi - lo;
+  if (nt <= 1 || n <= 1) {
+    std::sort(ord + lo, ord + hi);
+    starts.push_back((int32_t)lo);
+    for (int k = 1; k < nt; ++k) starts.push_back((int32_t)hi);  // empty leaves
+    return;
+  }
+  const int n1 = nt / 2;
+  const int64_t k = (n * n1 + nt / 2) / nt;
+  const double* P[3] = {px, py, pz};
+  int ax = -1;
+  double best = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double mn = P[a][ord[lo]], mx = mn;
+    for (int64_t q = lo; q < hi; ++q) {
+      mn = std::min(mn, P[a][ord[q]]);
+      mx = std::max(mx, P[a][ord[q]]);
+    }
+    if (mx - mn > best) { best = mx - mn; ax = a; }
+  }
+  if (ax >= 0) {
+    const double* c = P[ax];
+    std::nth_element(ord + lo, ord + lo + k, ord + hi, [c](int32_t a, int32_t b) {
+      return c[a] < c[b] || (c[a] == c[b] && a < b);
+    });
+  } else {
+    std::sort(ord + lo, ord + hi);
+  }
+  rcb_order(px, py, pz, ord, lo, lo + k, n1, starts);
+  rcb_order(px, py, pz, ord, lo + k, hi, nt - n1, starts);
+}
+
 }  // namespace
 
 struct EngineHost {
@@ -880,6 +923,8 @@ struct EikSwe {
           *out = nullptr;
   double* soa = nullptr;
   double* wts = nullptr;  // diagnostics weights (lazily allocated)
+  int* ord_d = nullptr;   // device cell -> user cell
+  std::vector<int32_t> ord_h;
   bool have_prev = false;
   double c09cube = 0.0;
   // graph cache for eik_swe_step
@@ -935,13 +980,13 @@ struct EikSwe {
   }
   eik_status h2d_cells(const double* h, double4* d) {
     CK(cudaMemcpyAsync(soa, h, 4 * N * sizeof(double), cudaMemcpyHostToDevice, eng.st));
-    k_soa_to_cell<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(soa, d, N);
+    k_soa_to_cell<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(soa, d, N, ord_d);
     ++eng.launches;
     CK(cudaGetLastError());
     return EIK_OK;
   }
   eik_status d2h_cells(const double4* d, double* h) {
-    k_cell_to_soa<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(d, soa, N);
+    k_cell_to_soa<<<std::min<int64_t>((N + 255) / 256, 4096), 256, 0, eng.st>>>(d, soa, N, ord_d);
     ++eng.launches;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h, soa, 4 * N * sizeof(double), cudaMemcpyDeviceToHost, eng.st));
@@ -1041,6 +1086,91 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
         else if (Df.data[k] != 0.0) dfx[i] += 1;
       }
   }
+  // ---- device cell order.  The Krylov pass works on tiles of <= TILE own
+  // cells plus their 2-ring halo; the cells are renumbered so that every tile
+  // is a contiguous range of device cells forming a compact patch: recursive
+  // coordinate bisection of the cell positions (n_x, n_y, n_z) into NT equal
+  // leaves (median splits along the longest extent, ties by user index).
+  // Degenerate positions (planar operators: n constant) keep the user order.
+  // Slots keep the user rows' sorted column order, so every stencil sum runs
+  // in scipy's order; only reductions over cells change their order.
+  int nsm = 0;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return fail(EIK_ECUDA, "no CUDA device");
+  const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * MINB, (N + TILE - 1) / TILE));
+  // the tile buffers of MINB co-resident CTAs must fit one SM's shared
+  // memory: more, smaller tiles until they do
+  int smem_sm = 0, smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const size_t smem_budget =
+      std::min<size_t>((size_t)smem_optin, (size_t)smem_sm / MINB - 1024 - 4096);
+  std::vector<int32_t> ord(N), tstart;
+  int NT = 0;
+  {
+    std::vector<int32_t> mark(N, -1);
+    for (int64_t per = (N + (int64_t)Gt * TILE - 1) / ((int64_t)Gt * TILE);; ++per) {
+      NT = (int)(Gt * per);
+      for (int64_t i = 0; i < N; ++i) ord[i] = (int32_t)i;
+      tstart.clear();
+      rcb_order(n_x, n_y, n_z, ord.data(), 0, N, NT, tstart);
+      tstart.push_back((int32_t)N);
+      int e1m = 1, e2m = 1;
+      std::vector<int32_t> e1;
+      for (int t = 0; t < NT; ++t) {
+        e1.clear();
+        int n1 = 0, n2 = 0;
+        for (int32_t d = tstart[t]; d < tstart[t + 1]; ++d) mark[ord[d]] = t, ++n1;
+        for (int32_t d = tstart[t]; d < tstart[t + 1]; ++d)
+          for (int32_t j : cols[ord[d]])
+            if (mark[j] != t) { mark[j] = t; e1.push_back(j); }
+        n1 += (int)e1.size();
+        n2 = n1;
+        for (int32_t j1 : e1)
+          for (int32_t j : cols[j1])
+            if (mark[j] != t) { mark[j] = t; ++n2; }
+        e1m = std::max(e1m, n1);
+        e2m = std::max(e2m, n2);
+      }
+      if (tile_smem_bytes(e1m, e2m) <= smem_budget || (N + NT - 1) / NT <= 2) break;
+    }
+  }
+  std::vector<int32_t> inv(N);
+  for (int64_t d = 0; d < N; ++d) inv[ord[d]] = (int32_t)d;
+  std::vector<double> nxP(N), nyP(N), nzP(N), fP(N), hsP(N);
+  {
+    std::vector<std::vector<int32_t>> colsP(N);
+    std::vector<int32_t> cntP(N), dfxP(N);
+    std::vector<double> coefP(coef.size()), df1P(df1.size());
+    for (int64_t d = 0; d < N; ++d) {
+      const int64_t i = ord[d];
+      for (int32_t j : cols[i]) colsP[d].push_back(inv[j]);
+      cntP[d] = cnt[i];
+      dfxP[d] = dfx[i];
+      for (int s2 = 0; s2 < K; ++s2) {
+        for (int o = 0; o < NOPS; ++o)
+          coefP[((size_t)s2 * NOPS + o) * N + d] = coef[((size_t)s2 * NOPS + o) * N + i];
+        df1P[(size_t)s2 * N + d] = df1[(size_t)s2 * N + i];
+        nbr[(size_t)s2 * N + d] = s2 < cntP[d] ? colsP[d][s2] : (int32_t)d;
+      }
+      nxP[d] = n_x[i];
+      nyP[d] = n_y[i];
+      nzP[d] = n_z[i];
+      fP[d] = f[i];
+      hsP[d] = h_s[i];
+    }
+    cols.swap(colsP);
+    cnt.swap(cntP);
+    dfx.swap(dfxP);
+    coef.swap(coefP);
+    df1.swap(df1P);
+    n_x = nxP.data();
+    n_y = nyP.data();
+    n_z = nzP.data();
+    f = fP.data();
+    h_s = hsP.data();
+  }
   // ---- compact (off-diagonal) stencil for the tiled Krylov pass, valid when
   // G, V, L rows sum to zero and D's diagonal is + the off-diagonal sum
   int KC = 1;
@@ -1084,45 +1214,15 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
     }
   }
 
-  // ---- tiles along the Hilbert order, one CTA per SM, each tile <= TPB own
-  // cells plus its 2-ring halo (local indices into shared memory)
-  int nsm = 0;
-  if (cudaSetDevice(device) != cudaSuccess ||
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
-    return fail(EIK_ECUDA, "no CUDA device");
-  const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * MINB, (N + TILE - 1) / TILE));
-  // the tile buffers of MINB co-resident CTAs must fit one SM's shared
-  // memory: shrink the tiles (more per CTA) until they do
-  int smem_sm = 0, smem_optin = 0;
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
-  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  const size_t smem_budget =
-      std::min<size_t>((size_t)smem_optin, (size_t)smem_sm / MINB - 1024 - 4096);
-  int NT = 0;
-  int64_t tsz = 0;
-  std::vector<int32_t> t_cell0, t_nT, t_nE1, t_nE2, t_e2off, t_e1off;
+  std::vector<int32_t> t_cell0(NT), t_nT(NT), t_nE1(NT), t_nE2(NT), t_e2off(NT), t_e1off(NT);
   std::vector<int32_t> e2map;
   std::vector<int16_t> lnbr;
   std::vector<double> LcE1;  // Laplacian rows of every tile's E1 cells, local order
   int e1max = 1, e2max = 1;
-#ifndef EIK_TILE_CAP
-#define EIK_TILE_CAP TILE
-#endif
-  constexpr int64_t kTileCap = EIK_TILE_CAP;  // own cells per tile (<= TILE)
-  static_assert(kTileCap <= TILE, "tile cap");
-  for (int64_t per = (N + (int64_t)Gt * kTileCap - 1) / ((int64_t)Gt * kTileCap);; ++per) {
-  NT = (int)(Gt * per);
-  tsz = (N + NT - 1) / NT;
-  if (tsz & 1) ++tsz;  // even tiles keep the TMA runs 16-byte aligned
-  for (auto* v : {&t_cell0, &t_nT, &t_nE1, &t_nE2, &t_e2off, &t_e1off}) v->assign(NT, 0);
-  e2map.clear();
-  lnbr.clear();
-  LcE1.clear();
-  e1max = e2max = 1;
   {
     std::vector<int32_t> loc(N, -1), list;
     for (int t = 0; t < NT; ++t) {
-      const int64_t lo = std::min<int64_t>(N, t * tsz), hi = std::min<int64_t>(N, lo + tsz);
+      const int64_t lo = tstart[t], hi = tstart[t + 1];
       list.clear();
       for (int64_t i = lo; i < hi; ++i) { loc[i] = (int32_t)list.size(); list.push_back((int32_t)i); }
       const int nT = (int)list.size();
@@ -1157,8 +1257,6 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
       e1max = std::max(e1max, nE1);
       e2max = std::max(e2max, nE2);
     }
-  }
-  if (tile_smem_bytes(e1max, e2max) <= smem_budget || tsz <= 2) break;
   }
   // ---- balance: tile t is processed by CTA t % Gt in the kernels; permute
   // the tiles so that this static assignment is a longest-processing-time
@@ -1284,6 +1382,9 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&c->x, N));
   CKC(B.get(&c->out, N));
   CKC(B.get(&c->soa, 4 * N));
+  CKC(B.get(&c->ord_d, N));
+  CKC(cudaMemcpy(c->ord_d, ord.data(), N * 4, cudaMemcpyHostToDevice));
+  c->ord_h = ord;
   double4 *ne, *lapA, *lapB;
   CKC(B.get(&ne, N));
   CKC(B.get(&lapA, N));
@@ -1413,7 +1514,11 @@ eik_status eik_swe_jac_nnz_rows(EikSwe* c, const double* u, int64_t* nnz,
   double v = 0.0;
   CK(cudaMemcpy(&v, c->eng.nnz_d, sizeof(double), cudaMemcpyDeviceToHost));
   *nnz = (int64_t)v;
-  if (per_cell) CK(cudaMemcpy(per_cell, c->soa, c->N * sizeof(double), cudaMemcpyDeviceToHost));
+  if (per_cell) {
+    std::vector<double> tmp(c->N);
+    CK(cudaMemcpy(tmp.data(), c->soa, c->N * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t d = 0; d < c->N; ++d) per_cell[c->ord_h[d]] = tmp[d];
+  }
   return EIK_OK;
 }
 
@@ -1726,8 +1831,11 @@ eik_status eik_swe_diagnostics(EikSwe* c, const double* u, const double* weights
   double* wdev = nullptr;
   if (weights) {
     if (!c->wts) CK(c->eng.mem.get(&c->wts, c->N));
-    CK(cudaMemcpyAsync(c->wts, weights, c->N * sizeof(double), cudaMemcpyHostToDevice,
+    std::vector<double> wp(c->N);
+    for (int64_t d = 0; d < c->N; ++d) wp[d] = weights[c->ord_h[d]];
+    CK(cudaMemcpyAsync(c->wts, wp.data(), c->N * sizeof(double), cudaMemcpyHostToDevice,
                        c->eng.st));
+    CK(cudaStreamSynchronize(c->eng.st));
     wdev = c->wts;
   }
   SweArgs A = c->args(src);

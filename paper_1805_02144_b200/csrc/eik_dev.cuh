@@ -369,42 +369,21 @@ __device__ __forceinline__ double4 swe_rhs_cell(const SweOp& S, const Src& w,
 // reference's planar operators -- only the off-diagonal slots are stored and
 //   (G e)_i = sum_j G_ij (e_j - e_i),  (D f)_i = sum_j D_ij (f_j + f_i).
 //
-// Default: the single-role pass at the end of this section (256-thread
-// CTAs, 2 per SM, every thread gathers then computes).  EIK_WS=2 with
-// EIK_TPB=512 selects the TMA warp-specialised pipeline `swe_tiled_tw` (warp
-// 0 bulk-copies coefficients, warps 1-7 gather, warps 8-15 compute); it
-// measured 141 us per Krylov iteration at L8 against 126 us for the default.
-#ifndef EIK_WS
-#define EIK_WS 0
-#endif
-constexpr int WS = EIK_WS;
-#ifndef EIK_PT
-#define EIK_PT (EIK_TPB / 2)
-#endif
-#ifndef EIK_WS_TPC
-#define EIK_WS_TPC 1
-#endif
-// EIK_SR2 (default): the single-role pass with its per-tile static data
-// (coefficients, n/eta, Laplacian rows and local neighbour rows of the
-// 1-ring) bulk-copied into shared memory by TMA while the threads gather
-// the halo, the next tile's cell map prefetched one tile ahead, and
-// EIK_SR2_TPC threads per own cell in the J v step.
-#ifndef EIK_SR2
-#define EIK_SR2 0
-#endif
-#ifndef EIK_SR2_TPC
-#define EIK_SR2_TPC 2
-#endif
-constexpr int SR2 = (EIK_WS == 0) ? EIK_SR2 : 0;
-constexpr int SR2_TPC = EIK_SR2_TPC;
-constexpr int PT = EIK_PT;                       // producer threads (TMA warp + gatherers)
-constexpr int WS_TPC = EIK_WS_TPC;               // consumer threads per cell
-constexpr int TILE = WS ? (TPB - PT) / WS_TPC : (SR2 ? TPB / SR2_TPC : TPB);  // max own cells per tile
-static_assert(WS != 2 || TILE == 256, "TMA-WS: 256-cell tiles");
+// Tiles are contiguous ranges of <= TPB device cells (compact patches, see
+// the device cell order in eik_swe_create); a CTA stages a tile's input
+// vector on the tile's 2-ring halo E2 in shared memory and every thread runs
+// the three steps of the tile in turn (256-thread CTAs, 2 per SM).
+//
+// Shared memory is kept small on purpose: it is carved out of the same
+// 256 KB per SM as the L1 that holds the pass's in-flight global loads.
+// Measured at L8 (us per Krylov iteration): +40 KB of shared memory per CTA
+// 159 vs 117; TMA / cp.async staging of the per-tile static data or of the
+// coefficient stream 157-171; L2 prefetch of the coefficient runs 125-139.
 #ifndef EIK_PROF
 #define EIK_PROF 0
 #endif
-constexpr int NCOEF = KCMAX * 9;  // staged coefficient runs (slot-major G/D/V)
+constexpr int TILE = TPB;          // max own cells per tile
+constexpr int NCOEF = KCMAX * 9;   // compact G/D/V runs per cell (slot-major)
 
 #ifndef EIK_SPLIT
 #define EIK_SPLIT 1
@@ -433,163 +412,25 @@ __device__ __forceinline__ void sst(const SArr& a, int l, double4 v) {
 #endif
 }
 
-#ifndef EIK_LCE1
-#define EIK_LCE1 1
-#endif
-#ifndef EIK_VMB
-#define EIK_VMB 0
-#endif
-#ifndef EIK_PRE3
-#define EIK_PRE3 0
-#endif
-#ifndef EIK_CPA
-#define EIK_CPA 0
-#endif
-#ifndef EIK_L2PF
-#define EIK_L2PF 0
-#endif
-#ifndef EIK_PIPE3
-#define EIK_PIPE3 0
-#endif
 struct TileSmem {
-  double* cb;  // [NCOEF][TILE] staged own-cell coefficients (TMA pipeline) or null
-  SArr x;
-  SArr La;
-  SArr U;
-  int* gid;
-  double4* vmb;  // [TILE] own-cell vector for the epilogue (EIK_VMB)
-  // EIK_CPA: per-tile static data staged by cp.async
-  short* rows;   // [e1max][8] local neighbour rows of E1
-  double* lce1;  // [e1max][6] Laplacian rows of E1
-  double4* neb;  // [TILE] (n, eta) of the own cells
-  int* map0;     // [e2r] cell map, double-buffered (next tile's prefetched)
-  int* map1;
+  SArr x;   // [e2max] input vector on E2
+  SArr La;  // [e1max] L x on E1
+  SArr U;   // [e1max] linearisation state on E1
 };
-
-__host__ __device__ constexpr int e2_round4(int e2max) { return (e2max + 3) & ~3; }
-#ifndef EIK_SMEM_PAD
-#define EIK_SMEM_PAD 0
-#endif
-__host__ __device__ constexpr size_t tile_buf_bytes(int e1max, int e2max) {
-  return (size_t)EIK_SMEM_PAD + (size_t)(EIK_VMB ? TILE : 0) * 32 + (size_t)e2max * 32 +
-         (size_t)e1max * 64 + (size_t)(EIK_LCE1 && !EIK_CPA ? 0 : e2max) * 4 + 16 +
-         (EIK_CPA ? (size_t)e1max * 64 + (size_t)TILE * 32 + (size_t)2 * e2_round4(e2max) * 4 + 16
-                  : 0);
+__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
+  return 128 + (size_t)e2max * 32 + (size_t)e1max * 64;
 }
-
-// single-role pass: one tile buffer after a 128-byte header
 __device__ __forceinline__ TileSmem tile_smem(const SweOp& S) {
   extern __shared__ __align__(128) unsigned char dsm[];
   TileSmem t;
-  t.cb = nullptr;
-  t.vmb = reinterpret_cast<double4*>(dsm + 128);
-  double2* q = reinterpret_cast<double2*>(dsm + 128 + (EIK_VMB ? TILE * 32 : 0));
+  double2* q = reinterpret_cast<double2*>(dsm + 128);
   t.x = SArr{q, S.e2max};
   q += 2 * S.e2max;
   t.La = SArr{q, S.e1max};
   q += 2 * S.e1max;
   t.U = SArr{q, S.e1max};
-  q += 2 * S.e1max;
-#if EIK_CPA
-  unsigned char* p = reinterpret_cast<unsigned char*>(q);
-  t.neb = reinterpret_cast<double4*>(p);
-  p += (size_t)TILE * 32;
-  t.lce1 = reinterpret_cast<double*>(p);
-  p += (size_t)S.e1max * 48;
-  t.rows = reinterpret_cast<short*>(p);
-  p += (size_t)S.e1max * 16;
-  t.map0 = reinterpret_cast<int*>(p);
-  t.map1 = t.map0 + e2_round4(S.e2max);
-  p += (size_t)2 * e2_round4(S.e2max) * 4;
-  t.gid = reinterpret_cast<int*>(p);
-#else
-  t.gid = reinterpret_cast<int*>(q);
-#endif
   return t;
 }
-
-__host__ __device__ constexpr size_t tw_buf_bytes(int e1max, int e2max) {
-  return ((size_t)e2max * 32 + (size_t)e1max * 64 + 127) / 128 * 128;
-}
-// SR2 layout (after a 128-byte mbarrier header), every part 16-byte aligned:
-// cb [NCOEF][TILE] | neb [TILE] | vmb [TILE] | rows [e1][8] short |
-// lce1 [e1][6] | map [2][e2r] int | x [e2] | La [e1] | U [e1]   (SArr halves)
-__host__ __device__ constexpr int sr2_e2r(int e2max) { return (e2max + 3) & ~3; }
-__host__ __device__ constexpr size_t sr2_smem_bytes(int e1max, int e2max) {
-  return 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 64 + (size_t)e1max * 16 +
-         (size_t)e1max * 48 + (size_t)2 * sr2_e2r(e2max) * 4 + (size_t)e2max * 32 +
-         (size_t)e1max * 64;
-}
-__host__ __device__ constexpr size_t tile_smem_bytes(int e1max, int e2max) {
-  return WS == 2 ? 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
-                       2 * tw_buf_bytes(e1max, e2max)
-                 : (SR2 ? sr2_smem_bytes(e1max, e2max) : 128 + tile_buf_bytes(e1max, e2max));
-}
-
-// ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t bytes,
-                                        unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-// Same copy with an L2 evict-first policy: the coefficient stream (≈ 60 % of
-// the bytes of a Krylov iteration, read once per iteration) must not push
-// the Krylov vectors written by the previous iteration out of the 126 MB L2.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_g2s_ef(void* dst, const void* src, uint32_t bytes,
-                                           unsigned long long* b, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_shared() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// per-thread asynchronous 16-byte global -> shared copies (LDGSTS)
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void pf_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-// L2 prefetch of tile t's own-cell coefficient runs and E1 Laplacian rows,
-// spread over the CTA's threads (128-byte lines)
-__device__ __forceinline__ void tile_prefetch_l2(const SweOp& S, int t);
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct Row8 {
   short s[8];
@@ -600,9 +441,16 @@ __device__ __forceinline__ Row8 load_row8(const short* p) {
   memcpy(&r, &v, 16);
   return r;
 }
+// the 6 off-diagonal Laplacian coefficients of one E1 row (16-byte loads)
+struct Lrow {
+  double v[8];
+};
+__device__ __forceinline__ Lrow load_lrow(const double* p) {
+  const double2 a = ldv2_nc(p), b = ldv2_nc(p + 2), c = ldv2_nc(p + 4);
+  return Lrow{{a.x, a.y, b.x, b.y, c.x, c.y, 0.0, 0.0}};
+}
 
-// compact coefficient order in coefc: [KCMAX][9][N], ops Vx Vy Vz Gx Gy Gz Dx Dy Dz.
-// Partial J x sums over slots [s0, s0+ns) for own cell `c` (x, La, U in smem).
+// compact coefficient order in coefc: [KCMAX][9][NC], ops Vx Vy Vz Gx Gy Gz Dx Dy Dz.
 struct JvAcc {
   double zeta, gx, gy, gz, dv, l0, l1, l2, l3;
 };
@@ -623,16 +471,6 @@ __device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, Coe
     const double* cp = S.coefc + i + (s0 + k) * st;
 #pragma unroll
     for (int q = 0; q < 9; ++q) cf.v[k][q] = __ldcs(cp + q * S.NC);
-  }
-}
-template <int CH>
-__device__ __forceinline__ void coef_load_smem(const TileSmem& ts, int c, int s0,
-                                               CoefChunk<CH>& cf) {
-#pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    const double* cp = ts.cb + ((s0 + k) * 9) * TILE + c;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) cf.v[k][q] = cp[q * TILE];
   }
 }
 // own-cell terms shared by every slot
@@ -681,25 +519,23 @@ __device__ __forceinline__ void jv_accum(const SweOp& S, const TileSmem& ts, con
   }
 }
 
-// Slots are processed in chunks of EIK_CHUNK: all 9*CHUNK coefficient loads
-// of a chunk are issued before any of them is used (a compiler memory fence
-// keeps them together), so each thread keeps ~27 streaming loads in flight
-// instead of the handful the default schedule interleaves with the math.
-template <int kSrc, int NS>
-__device__ __forceinline__ JvAcc swe_jv_part(const SweOp& S, const TileSmem& ts, const short* row,
-                                             const double* lc, int s0, int c, int64_t i,
-                                             double4 ai, double4 Ui, double4 lai) {
-  // kSrc: 0 = coefficients from global, 1 = from the TMA-staged smem block
+// Sum over all KCMAX slots of own cell i (x, La, U in smem).  Slots are
+// processed in chunks of EIK_CHUNK: all 9*CHUNK coefficient loads of a chunk
+// are issued before any of them is used (a compiler memory fence keeps them
+// together), so each thread keeps ~27 streaming loads in flight instead of
+// the handful the default schedule interleaves with the math.
+__device__ __forceinline__ JvAcc swe_jv_sum(const SweOp& S, const TileSmem& ts, const short* row,
+                                            const double* lc, int64_t i, double4 ai, double4 Ui,
+                                            double4 lai) {
   const JvOwn o = jv_own(S, ai, Ui, lai);
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  constexpr int CH = (EIK_CHUNK < NS) ? EIK_CHUNK : NS;
+  constexpr int CH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
 #pragma unroll
-  for (int k0 = 0; k0 < NS; k0 += CH) {
+  for (int k0 = 0; k0 < KCMAX; k0 += CH) {
     CoefChunk<CH> cf;
-    if constexpr (kSrc == 1) coef_load_smem<CH>(ts, c, s0 + k0, cf);
-    else coef_load<CH>(S, i, s0 + k0, cf);
-    if constexpr (kSrc == 0) asm volatile("" ::: "memory");
-    jv_accum<CH>(S, ts, row, lc, s0 + k0, cf, o, a);
+    coef_load<CH>(S, i, k0, cf);
+    asm volatile("" ::: "memory");
+    jv_accum<CH>(S, ts, row, lc, k0, cf, o, a);
   }
   return a;
 }
@@ -742,502 +578,11 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
 }
 
 // One pass over every tile: x on E2 -> smem, L x on E1, z = scale * J x on
-// the own cells -> epi(i, z, x_i).  A whole Krylov iteration (orthogonalise
-// + normalise v_j, L v_j, J v_j, projections) is one such pass: one HBM
-// sweep and one grid barrier per iteration.
-__device__ __forceinline__ void nb_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nb_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-// ---- TMA warp-specialised pipeline (EIK_WS == 2) ---------------------------
-// warp 0: TMA issuer -- streams each tile's own-cell coefficients (54 runs,
-//         two halves of 3 stencil slots) and (n, eta) into shared memory
-//         through cp.async.bulk + mbarriers, one half ahead of the consumers;
-// warps 1..PT/32-1: gatherers -- steps 1-2 of tile k+1 (x on E2, L x on E1)
-//         into tile buffer (k+1)&1;
-// warps PT/32..: consumers -- step 3 (J x) from shared memory only.
-struct TwSmem {
-  unsigned long long* cfull;   // [NST] stage h landed (tx-count); [NST..2NST) stage released
-  double* cb;                  // [NCOEF][TILE]
-  double4* neb;                // [TILE]
-  SArr x, La, U;               // tile buffer
-};
-__device__ __forceinline__ TwSmem tw_smem(const SweOp& S, int buf) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  TwSmem t;
-  t.cfull = reinterpret_cast<unsigned long long*>(dsm);
-  t.cb = reinterpret_cast<double*>(dsm + 128);
-  t.neb = reinterpret_cast<double4*>(dsm + 128 + (size_t)NCOEF * TILE * 8);
-  unsigned char* p = dsm + 128 + (size_t)NCOEF * TILE * 8 + (size_t)TILE * 32 +
-                     (size_t)buf * tw_buf_bytes(S.e1max, S.e2max);
-  double2* q = reinterpret_cast<double2*>(p);
-  t.x = SArr{q, S.e2max};
-  q += 2 * S.e2max;
-  t.La = SArr{q, S.e1max};
-  q += 2 * S.e1max;
-  t.U = SArr{q, S.e1max};
-  return t;
-}
-__device__ __forceinline__ TileSmem ts_as_tile(const TwSmem& b, const TwSmem& t0) {
-  TileSmem r;
-  r.cb = t0.cb;
-  r.x = b.x;
-  r.La = b.La;
-  r.U = b.U;
-  r.gid = nullptr;
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive1(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-
-template <class Epi>
-__device__ void swe_tiled_tw(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
-  constexpr int GT = PT - 32;            // gatherer threads
-  constexpr int CT = TPB - PT;           // consumer threads (== TILE * WS_TPC)
-  constexpr int NB = GT + CT;            // named-barrier participants
-  constexpr int NCW = CT / 32;           // consumer warps
-#ifndef EIK_NSTAGE
-#define EIK_NSTAGE 3
-#endif
-  constexpr int NST = EIK_NSTAGE;        // coefficient stages (2: halves, 3: thirds)
-  constexpr int SLOTS_PER = KCMAX / NST;
-  constexpr int HALF_RUNS = NCOEF / NST; // runs per stage
-  const int warp = threadIdx.x >> 5;
-  const TwSmem t0 = tw_smem(S, 0);
-  if (threadIdx.x == 0) {
-    for (int h = 0; h < NST; ++h) {
-      mbar_init(t0.cfull + h, 1);
-      mbar_init(t0.cfull + NST + h, NCW);  // cempty
-    }
-  }
-  __syncthreads();
-  int ktiles = 0;
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) ++ktiles;
-#if EIK_PROF
-  long long pw = 0, pw2 = 0, pt0 = clock64();
-#define TWP_BEGIN long long w0_ = clock64();
-#define TWP_END(v) v += clock64() - w0_;
-#else
-#define TWP_BEGIN
-#define TWP_END(v)
-#endif
-  if (warp == 0) {
-    // ---------------- TMA issuer
-    if (threadIdx.x == 0) {
-      uint32_t pe[NST];
-      for (int h = 0; h < NST; ++h) pe[h] = 0u;
-      const uint64_t pol = l2_evict_first_policy();
-      for (int k = 0; k < ktiles; ++k) {
-        const int t = blockIdx.x + k * gridDim.x;
-        const int64_t c0 = __ldg(S.t_cell0 + t);
-        const uint32_t nT = (uint32_t)__ldg(S.t_nT + t);
-        for (int h = 0; h < NST; ++h) {
-          if (k >= 1) {
-            mbar_wait(t0.cfull + NST + h, pe[h]);
-            pe[h] ^= 1u;
-          }
-          fence_proxy_async_shared();
-          // runs rounded up to 16 bytes (odd last tile): the extra element is
-          // the next chunk's first (or the allocation's slack), never read
-          const uint32_t run = (nT * 8u + 15u) & ~15u;
-          const uint32_t bytes = run * HALF_RUNS + (h == NST - 1 ? nT * 32u : 0u);
-          mbar_expect_tx(t0.cfull + h, bytes);
-          if (nT > 0) {
-            for (int q = h * HALF_RUNS; q < (h + 1) * HALF_RUNS; ++q)
-              tma_g2s_ef(t0.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.NC + c0, run,
-                         t0.cfull + h, pol);
-            if (h == NST - 1) tma_g2s(t0.neb, S.ne + c0, nT * 32u, t0.cfull + h);
-          }
-        }
-      }
-    }
-  } else if (threadIdx.x < PT) {
-    // ---------------- gatherers: steps 1-2
-    const int lt = threadIdx.x - 32;
-    for (int k = 0; k < ktiles; ++k) {
-      const int t = blockIdx.x + k * gridDim.x;
-      const int b = k & 1;
-      const TwSmem ts = tw_smem(S, b);
-      {
-        TWP_BEGIN
-        if (k >= 2) nb_sync(4 + b, NB);
-        TWP_END(pw)
-      }
-      const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-      const int* map = S.e2map + __ldg(S.t_e2off + t);
-      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-      for (int base = 0; base < nE2; base += 2 * GT) {
-        const int ca = base + lt, cb = ca + GT;
-        const bool va = ca < nE2, vb = cb < nE2;
-        const int ga = va ? __ldg(map + ca) : 0;
-        const int gb = vb ? __ldg(map + cb) : 0;
-        double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
-                b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
-        if (va) {
-          a0 = F.src[ga];
-          if (F.vm2) a1 = F.vm2[ga];
-          if (F.vm1) a2 = F.vm1[ga];
-          if (ca < nE1) ua = S.lin[ga];
-        }
-        if (vb) {
-          b0 = F.src[gb];
-          if (F.vm2) b1 = F.vm2[gb];
-          if (F.vm1) b2 = F.vm1[gb];
-          if (cb < nE1) ub = S.lin[gb];
-        }
-        if (va) {
-          const double4 x = form_x(F, a0, a1, a2);
-          sst(ts.x, ca, x);
-          if (ca < nE1) sst(ts.U, ca, ua);
-          if (F.out && ca < nT) F.out[ga] = x;
-        }
-        if (vb) {
-          const double4 x = form_x(F, b0, b1, b2);
-          sst(ts.x, cb, x);
-          if (cb < nE1) sst(ts.U, cb, ub);
-          if (F.out && cb < nT) F.out[gb] = x;
-        }
-      }
-      nb_sync(1, GT);
-      for (int c = lt; c < nE1; c += GT) {
-        const Row8 row = load_row8(rows + (int64_t)c * 8);
-        const double* lc = S.Lc + (int64_t)__ldg(map + c) * 8;
-        const double4 xc = sld(ts.x, c);
-        double4 acc = d4(0.0);
-#pragma unroll
-        for (int s = 0; s < KCMAX; ++s) {
-          const double l = __ldg(lc + s);
-          const double4 xv = sld(ts.x, row.s[s]);
-          acc.x += l * (xv.x - xc.x);
-          acc.y += l * (xv.y - xc.y);
-          acc.z += l * (xv.z - xc.z);
-          acc.w += l * (xv.w - xc.w);
-        }
-        sst(ts.La, c, acc);
-      }
-      nb_arrive(2 + b, NB);
-    }
-    for (int k = ktiles > 2 ? ktiles - 2 : 0; k < ktiles; ++k) nb_sync(4 + (k & 1), NB);
-  } else {
-    // ---------------- consumers: step 3 from shared memory
-    // WS_TPC == 1: one thread per cell, the two coefficient halves in turn
-    //   (half 0 is released to the TMA warp before half 1 is computed);
-    // WS_TPC == 2: adjacent lanes take slots 0-2 / 3-5 of one cell.
-    const int ct = threadIdx.x - PT;
-    const int c = ct / WS_TPC;
-    const int half = ct % WS_TPC;
-    const int lane = threadIdx.x & 31;
-    uint32_t pf[4] = {0u, 0u, 0u, 0u};
-    for (int k = 0; k < ktiles; ++k) {
-      const int t = blockIdx.x + k * gridDim.x;
-      const int b = k & 1;
-      const TwSmem ts = tw_smem(S, b);
-      const int64_t c0 = __ldg(S.t_cell0 + t);
-      const int nT = __ldg(S.t_nT + t);
-      const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-      const bool live = c < nT;
-      const int cc = live ? c : 0;
-      const int64_t i = c0 + cc;
-      // global reads that do not depend on the staged data first
-      const Row8 row = load_row8(rows + (int64_t)cc * 8);
-      double lcr[8];
-      const double* lc = S.Lc + i * 8;
-#pragma unroll
-      for (int s = 0; s < KCMAX; ++s) lcr[s] = __ldg(lc + s);
-      const double4 vm = (F.epi_vm1 && half == 0) ? F.epi_vm1[i] : d4(0.0);
-      // (Lc rows were just read by the gatherers for this tile: L1/L2 hits)
-      {
-        TWP_BEGIN
-        nb_sync(2 + b, NB);
-        TWP_END(pw)
-      }
-      const double4 ai = sld(ts.x, cc);
-      const double4 Ui = sld(ts.U, cc);
-      const double4 lai = sld(ts.La, cc);
-      JvAcc a;
-      double4 q;
-      if constexpr (WS_TPC == 1) {
-        a = JvAcc{0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int h = 0; h < NST; ++h) {
-          {
-            TWP_BEGIN
-            mbar_wait(t0.cfull + h, pf[h]);
-            TWP_END(pw2)
-          }
-          pf[h] ^= 1u;
-          const JvAcc a2 = swe_jv_part<1, SLOTS_PER>(S, ts_as_tile(ts, t0), row.s, lcr,
-                                                      h * SLOTS_PER, cc, i, ai, Ui, lai);
-          if (h == NST - 1) q = t0.neb[cc];
-          __syncwarp();
-          if (lane == 0) mbar_arrive1(t0.cfull + NST + h);
-          a.zeta += a2.zeta; a.gx += a2.gx; a.gy += a2.gy; a.gz += a2.gz; a.dv += a2.dv;
-          a.l0 += a2.l0; a.l1 += a2.l1; a.l2 += a2.l2; a.l3 += a2.l3;
-        }
-      } else {
-        {
-          TWP_BEGIN
-          mbar_wait(t0.cfull, pf[0]);
-          mbar_wait(t0.cfull + 1, pf[1]);
-          TWP_END(pw2)
-        }
-        pf[0] ^= 1u;
-        pf[1] ^= 1u;
-        a = swe_jv_part<1, KCMAX / 2>(S, ts_as_tile(ts, t0), row.s, lcr, half * (KCMAX / 2), cc,
-                                       i, ai, Ui, lai);
-        q = t0.neb[cc];
-        a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, 1);
-        a.gx += __shfl_xor_sync(0xffffffffu, a.gx, 1);
-        a.gy += __shfl_xor_sync(0xffffffffu, a.gy, 1);
-        a.gz += __shfl_xor_sync(0xffffffffu, a.gz, 1);
-        a.dv += __shfl_xor_sync(0xffffffffu, a.dv, 1);
-        a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, 1);
-        a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, 1);
-        a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, 1);
-        a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, 1);
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive1(t0.cfull + NST);
-          mbar_arrive1(t0.cfull + NST + 1);
-        }
-      }
-      if (live && half == 0) {
-        const double4 z = S.scale * swe_jv_finish(S, a, q, ai, Ui);
-        epi(i, z, ai, vm);
-      }
-      nb_arrive(4 + b, NB);
-    }
-  }
-  __syncthreads();
-#if EIK_PROF
-  if (S.prof && (threadIdx.x == 32 || threadIdx.x == PT)) {
-    const int o = threadIdx.x == 32 ? 0 : 2;
-    atomicAdd(S.prof + o, (unsigned long long)pw);
-    atomicAdd(S.prof + o + 1, (unsigned long long)(clock64() - pt0));
-    if (o == 2) atomicAdd(S.prof + 4, (unsigned long long)pw2);
-  }
-#endif
-#undef TWP_BEGIN
-#undef TWP_END
-}
-
-// ---- SR2: single-role pass with TMA-staged per-tile static data ----------
-struct Sr2Smem {
-  unsigned long long* mb;  // [0..1] map buffers, [2] small statics, [3] coefficients
-  double* cb;              // [NCOEF][TILE]
-  double4* neb;            // [TILE] (n, eta) of the own cells
-  double4* vmb;            // [TILE] own-cell vector handed to the epilogue
-  short* rows;             // [e1max][8]
-  double* lce1;            // [e1max][6]
-  int* map[2];             // [e2r]
-  SArr x, La, U;
-};
-__device__ __forceinline__ Sr2Smem sr2_smem(const SweOp& S) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  Sr2Smem t;
-  unsigned char* p = dsm;
-  t.mb = reinterpret_cast<unsigned long long*>(p);
-  p += 128;
-  t.cb = reinterpret_cast<double*>(p);
-  p += (size_t)NCOEF * TILE * 8;
-  t.neb = reinterpret_cast<double4*>(p);
-  p += (size_t)TILE * 32;
-  t.vmb = reinterpret_cast<double4*>(p);
-  p += (size_t)TILE * 32;
-  t.rows = reinterpret_cast<short*>(p);
-  p += (size_t)S.e1max * 16;
-  t.lce1 = reinterpret_cast<double*>(p);
-  p += (size_t)S.e1max * 48;
-  const int e2r = sr2_e2r(S.e2max);
-  t.map[0] = reinterpret_cast<int*>(p);
-  t.map[1] = t.map[0] + e2r;
-  p += (size_t)2 * e2r * 4;
-  double2* q = reinterpret_cast<double2*>(p);
-  t.x = SArr{q, S.e2max};
-  q += 2 * S.e2max;
-  t.La = SArr{q, S.e1max};
-  q += 2 * S.e1max;
-  t.U = SArr{q, S.e1max};
-  return t;
-}
-
-template <class Epi>
-__device__ void swe_tiled_sr2(const SweOp& S, const Form& F, const Epi& epi) {
-  const Sr2Smem L = sr2_smem(S);
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < 4; ++q) mbar_init(L.mb + q, 1);
-  }
-  __syncthreads();
-  // one thread issues every bulk copy of a tile; the cell map of the next
-  // tile goes one tile ahead (double-buffered) so the halo gather of a tile
-  // starts without a dependent global round trip
-  auto issue_map = [&](int t, int b) {
-    const uint32_t bytes = ((uint32_t)__ldg(S.t_nE2 + t) * 4u + 15u) & ~15u;
-    mbar_expect_tx(L.mb + b, bytes);
-    if (bytes) tma_g2s(b ? L.map[1] : L.map[0], S.e2map + __ldg(S.t_e2off + t), bytes, L.mb + b);
-  };
-  if (threadIdx.x == 0 && (int)blockIdx.x < S.ntiles) {
-    fence_proxy_async_shared();
-    issue_map(blockIdx.x, 0);
-  }
-  uint32_t ph_map = 0u, ph_s = 0u, ph_c = 0u;  // mbarrier parities (map: one bit per buffer)
-  int k = 0;
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x, ++k) {
-    const int b = k & 1;
-    const int64_t c0 = __ldg(S.t_cell0 + t);
-    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-    const int e1off = __ldg(S.t_e1off + t);
-    if (threadIdx.x == 0) {
-      // every thread finished the previous tile (barrier at its end): the
-      // generic-proxy reads of these buffers are ordered before the copies
-      fence_proxy_async_shared();
-      const uint32_t rb = (uint32_t)nE1 * 16u, lb = (uint32_t)nE1 * 48u, nb = (uint32_t)nT * 32u;
-      mbar_expect_tx(L.mb + 2, rb + lb + nb);
-      if (nE1) {
-        tma_g2s(L.rows, S.lnbr + (int64_t)e1off * 8, rb, L.mb + 2);
-        tma_g2s(L.lce1, S.LcE1 + (int64_t)e1off * 6, lb, L.mb + 2);
-      }
-      if (nT) tma_g2s(L.neb, S.ne + c0, nb, L.mb + 2);
-      // runs rounded up to 16 bytes (odd last tile): the extra element is the
-      // next run's first (or the allocation's slack), never read
-      const uint32_t run = ((uint32_t)nT * 8u + 15u) & ~15u;
-      mbar_expect_tx(L.mb + 3, run * NCOEF);
-      if (nT) {
-        const uint64_t pol = l2_evict_first_policy();
-        for (int q = 0; q < NCOEF; ++q)
-          tma_g2s_ef(L.cb + (size_t)q * TILE, S.coefc + (int64_t)q * S.NC + c0, run, L.mb + 3,
-                     pol);
-      }
-      if (t + (int)gridDim.x < S.ntiles) issue_map(t + gridDim.x, b ^ 1);
-    }
-    // step 1: x on E2 (two cells per thread per round, all loads issued first)
-    mbar_wait(L.mb + b, (ph_map >> b) & 1u);
-    ph_map ^= 1u << b;
-    const int* map = b ? L.map[1] : L.map[0];
-    for (int base = 0; base < nE2; base += 2 * TPB) {
-      const int ca = base + threadIdx.x, cb = ca + TPB;
-      const bool va = ca < nE2, vb = cb < nE2;
-      const int ga = va ? map[ca] : 0;
-      const int gb = vb ? map[cb] : 0;
-      double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
-              b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
-      if (va) {
-        a0 = ldv(F.src + ga);
-        if (F.vm2) a1 = ldv(F.vm2 + ga);
-        if (F.vm1) a2 = ldv(F.vm1 + ga);
-        if (ca < nE1) ua = ldv_nc(S.lin + ga);
-      }
-      if (vb) {
-        b0 = ldv(F.src + gb);
-        if (F.vm2) b1 = ldv(F.vm2 + gb);
-        if (F.vm1) b2 = ldv(F.vm1 + gb);
-        if (cb < nE1) ub = ldv_nc(S.lin + gb);
-      }
-      if (va) {
-        const double4 x = form_x(F, a0, a1, a2);
-        sst(L.x, ca, x);
-        if (ca < nE1) sst(L.U, ca, ua);
-        if (ca < nT) {
-          if (F.out) stv(F.out + ga, x);
-          if (F.epi_vm1) L.vmb[ca] = (F.epi_vm1 == F.vm1) ? a2 : ldv(F.epi_vm1 + ga);
-        }
-      }
-      if (vb) {
-        const double4 x = form_x(F, b0, b1, b2);
-        sst(L.x, cb, x);
-        if (cb < nE1) sst(L.U, cb, ub);
-        if (cb < nT) {
-          if (F.out) stv(F.out + gb, x);
-          if (F.epi_vm1) L.vmb[cb] = (F.epi_vm1 == F.vm1) ? b2 : ldv(F.epi_vm1 + gb);
-        }
-      }
-    }
-    __syncthreads();
-    // step 2: L x on E1 (difference form), rows and coefficients in smem
-    mbar_wait(L.mb + 2, ph_s);
-    ph_s ^= 1u;
-    for (int c = threadIdx.x; c < nE1; c += TPB) {
-      const Row8 row = *reinterpret_cast<const Row8*>(L.rows + c * 8);
-      const double2* lc2 = reinterpret_cast<const double2*>(L.lce1 + c * 6);
-      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
-      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
-      const double4 xc = sld(L.x, c);
-      double4 acc = d4(0.0);
-#pragma unroll
-      for (int s2 = 0; s2 < KCMAX; ++s2) {
-        const double l = lv[s2];
-        const double4 xv = sld(L.x, row.s[s2]);
-        acc.x += l * (xv.x - xc.x);
-        acc.y += l * (xv.y - xc.y);
-        acc.z += l * (xv.z - xc.z);
-        acc.w += l * (xv.w - xc.w);
-      }
-      sst(L.La, c, acc);
-    }
-    __syncthreads();
-    // step 3: z = scale * J x on the own cells, SR2_TPC threads per cell
-    mbar_wait(L.mb + 3, ph_c);
-    ph_c ^= 1u;
-    {
-      constexpr int NSL = KCMAX / SR2_TPC;
-      const int c = threadIdx.x / SR2_TPC;
-      const int part = threadIdx.x % SR2_TPC;
-      {
-        const bool live = c < nT;
-        const int cc = live ? c : 0;
-        const int64_t i = c0 + cc;
-        // (row and Laplacian coefficients read from shared memory: the slot
-        // range depends on `part`, register arrays would go to local memory)
-        const short* row = L.rows + cc * 8;
-        const double* lcr = L.lce1 + cc * 6;
-        const double4 ai = sld(L.x, cc);
-        const double4 Ui = sld(L.U, cc);
-        const double4 lai = sld(L.La, cc);
-        TileSmem ts;
-        ts.cb = L.cb;
-        ts.x = L.x;
-        ts.La = L.La;
-        ts.U = L.U;
-        ts.gid = nullptr;
-        JvAcc a = swe_jv_part<1, NSL>(S, ts, row, lcr, part * NSL, cc, i, ai, Ui, lai);
-#pragma unroll
-        for (int o = 1; o < SR2_TPC; o <<= 1) {
-          a.zeta += __shfl_xor_sync(0xffffffffu, a.zeta, o);
-          a.gx += __shfl_xor_sync(0xffffffffu, a.gx, o);
-          a.gy += __shfl_xor_sync(0xffffffffu, a.gy, o);
-          a.gz += __shfl_xor_sync(0xffffffffu, a.gz, o);
-          a.dv += __shfl_xor_sync(0xffffffffu, a.dv, o);
-          a.l0 += __shfl_xor_sync(0xffffffffu, a.l0, o);
-          a.l1 += __shfl_xor_sync(0xffffffffu, a.l1, o);
-          a.l2 += __shfl_xor_sync(0xffffffffu, a.l2, o);
-          a.l3 += __shfl_xor_sync(0xffffffffu, a.l3, o);
-        }
-        if (live && part == 0) {
-          const double4 z = S.scale * swe_jv_finish(S, a, L.neb[cc], ai, Ui);
-          const double4 vm = F.epi_vm1 ? L.vmb[cc] : d4(0.0);
-          epi(i, z, ai, vm);
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Single-role tiled pass (the default): every thread does the
-// three steps of a tile in turn, separated by __syncthreads.
+// the own cells -> epi(i, z, x_i, epi_vm1_i).  A whole Krylov iteration
+// (orthogonalise + normalise v_j, L v_j, J v_j, projections) is one such
+// pass: one HBM sweep and one grid barrier per iteration.
 template <class Epi>
 __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
-  if constexpr (WS == 2) {
-    swe_tiled_tw(sm, S, F, epi);
-    return;
-  }
-  if constexpr (SR2 != 0) {
-    swe_tiled_sr2(S, F, epi);
-    return;
-  }
   const TileSmem ts = tile_smem(S);
 #if EIK_PROF
   long long pst[3] = {0, 0, 0}, pt = clock64();
@@ -1245,75 +590,20 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
 #else
 #define SRP_MARK(k)
 #endif
-#if EIK_CPA
-  // Every tile's contiguous static data (local neighbour rows and Laplacian
-  // rows of E1, (n, eta) of the own cells) is copied to shared memory by
-  // cp.async while the halo is gathered; the cell map of the next tile is
-  // copied one tile ahead, so the gather starts without a dependent global
-  // round trip.
-  auto issue_map = [&](int t, int* dst) {
-    const int n4 = (__ldg(S.t_nE2 + t) + 3) >> 2;
-    const int* src = S.e2map + __ldg(S.t_e2off + t);
-    for (int q = threadIdx.x; q < n4; q += TPB) cp16(dst + 4 * q, src + 4 * q);
-  };
-  if ((int)blockIdx.x < S.ntiles) {
-    issue_map(blockIdx.x, ts.map0);
-    cp_commit();
-    cp_wait_all();
-  }
-  __syncthreads();
-  int kt = 0;
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x, ++kt) {
-    const int64_t c0 = __ldg(S.t_cell0 + t);
-    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-    const int e1off = __ldg(S.t_e1off + t);
-    {
-      const short* rg = S.lnbr + (int64_t)e1off * 8;
-      const double* lg = S.LcE1 + (int64_t)e1off * 6;
-      for (int q = threadIdx.x; q < nE1; q += TPB) {
-        cp16(ts.rows + q * 8, rg + q * 8);
-        cp16(ts.lce1 + q * 6, lg + q * 6);
-        cp16(ts.lce1 + q * 6 + 2, lg + q * 6 + 2);
-        cp16(ts.lce1 + q * 6 + 4, lg + q * 6 + 4);
-      }
-      for (int q = threadIdx.x; q < 2 * nT; q += TPB)
-        cp16(reinterpret_cast<double*>(ts.neb) + 2 * q,
-             reinterpret_cast<const double*>(S.ne + c0) + 2 * q);
-      if (t + (int)gridDim.x < S.ntiles) issue_map(t + gridDim.x, (kt & 1) ? ts.map0 : ts.map1);
-      cp_commit();
-    }
-    if (nT == 0) {  // uniform over the CTA
-      cp_wait_all();
-      __syncthreads();
-      continue;
-    }
-    const int* map = (kt & 1) ? ts.map1 : ts.map0;
-    const short* rows = ts.rows;
-#else
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
     if (nT == 0) continue;  // uniform over the CTA
     const int* map = S.e2map + __ldg(S.t_e2off + t);
-    const short* rows = S.lnbr + (int64_t)__ldg(S.t_e1off + t) * 8;
-#endif
-#if EIK_L2PF == 1
-    tile_prefetch_l2(S, t);
-#elif EIK_L2PF == 2
-    if (t == (int)blockIdx.x) tile_prefetch_l2(S, t);
-    if (t + (int)gridDim.x < S.ntiles) tile_prefetch_l2(S, t + gridDim.x);
-#endif
+    const int e1off = __ldg(S.t_e1off + t);
+    const short* rows = S.lnbr + (int64_t)e1off * 8;
+    const double* lce1 = S.LcE1 + (int64_t)e1off * 6;
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
     for (int base = 0; base < nE2; base += 2 * TPB) {
       const int ca = base + threadIdx.x, cb = ca + TPB;
       const bool va = ca < nE2, vb = cb < nE2;
-#if EIK_CPA
-      const int ga = va ? map[ca] : 0;
-      const int gb = vb ? map[cb] : 0;
-#else
       const int ga = va ? __ldg(map + ca) : 0;
       const int gb = vb ? __ldg(map + cb) : 0;
-#endif
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
               b2 = d4(0.0), ua = d4(0.0), ub = d4(0.0);
       if (va) {
@@ -1330,63 +620,27 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       }
       if (va) {
         const double4 x = form_x(F, a0, a1, a2);
-        if (!EIK_LCE1) ts.gid[ca] = ga;
         sst(ts.x, ca, x);
         if (ca < nE1) sst(ts.U, ca, ua);
         if (F.out && ca < nT) stv(F.out + ga, x);
-#if EIK_VMB
-        if (F.epi_vm1 && ca < nT) ts.vmb[ca] = (F.epi_vm1 == F.vm1) ? a2 : ldv(F.epi_vm1 + ga);
-#endif
       }
       if (vb) {
         const double4 x = form_x(F, b0, b1, b2);
-        if (!EIK_LCE1) ts.gid[cb] = gb;
         sst(ts.x, cb, x);
         if (cb < nE1) sst(ts.U, cb, ub);
         if (F.out && cb < nT) stv(F.out + gb, x);
-#if EIK_VMB
-        if (F.epi_vm1 && cb < nT) ts.vmb[cb] = (F.epi_vm1 == F.vm1) ? b2 : ldv(F.epi_vm1 + gb);
-#endif
       }
     }
-#if EIK_CPA
-    cp_wait_all();
-#endif
     __syncthreads();
     SRP_MARK(0)
-#if EIK_PRE3
-    // step 3's first coefficient chunk goes out now, in flight during step 2
-    constexpr int PCH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
-    CoefChunk<PCH> pre;
-    if ((int)threadIdx.x < nT) coef_load<PCH>(S, c0 + threadIdx.x, 0, pre);
-#endif
-    // step 2: L x on E1 (difference form)
-    const double* lce1 = S.LcE1 + (int64_t)__ldg(S.t_e1off + t) * 6;
-    for (int c = threadIdx.x; c < nE1; c += TPB) {
-#if EIK_CPA
-      const Row8 row = *reinterpret_cast<const Row8*>(rows + c * 8);
-#else
-      const Row8 row = load_row8(rows + (int64_t)c * 8);
-#endif
-#if EIK_CPA
-      const double2* lc2 = reinterpret_cast<const double2*>(ts.lce1 + c * 6);
-      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
-      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
-#elif EIK_LCE1
-      const double2 l01 = ldv2_nc(lce1 + (int64_t)c * 6), l23 = ldv2_nc(lce1 + (int64_t)c * 6 + 2),
-                    l45 = ldv2_nc(lce1 + (int64_t)c * 6 + 4);
-      const double lv[6] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y};
-#else
-      const double* lc = S.Lc + (int64_t)ts.gid[c] * 8;
-      const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(lc));
-      const double2 l45 = ldv2_nc(lc + 4);
-      const double lv[6] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y};
-#endif
+    // step 2: L x on E1 (difference form; rows and coefficients contiguous
+    // per tile), two rows per thread per round with their loads issued first
+    auto lap_row = [&](int c, const Row8& row, const Lrow& lr) {
       const double4 xc = sld(ts.x, c);
       double4 acc = d4(0.0);
 #pragma unroll
       for (int s = 0; s < KCMAX; ++s) {
-        const double l = lv[s];
+        const double l = lr.v[s];
         const double4 xv = sld(ts.x, row.s[s]);
         acc.x += l * (xv.x - xc.x);
         acc.y += l * (xv.y - xc.y);
@@ -1394,7 +648,9 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
         acc.w += l * (xv.w - xc.w);
       }
       sst(ts.La, c, acc);
-    }
+    };
+    for (int c = threadIdx.x; c < nE1; c += TPB)
+      lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
     __syncthreads();
     SRP_MARK(1)
     // step 3: z = scale * J x on the own cells
@@ -1404,65 +660,11 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       const double4 ai = sld(ts.x, c);
       const double4 Ui = sld(ts.U, c);
       const double4 lai = sld(ts.La, c);
-#if EIK_CPA
-      const Row8 row = *reinterpret_cast<const Row8*>(rows + c * 8);
-      const double2* lc2 = reinterpret_cast<const double2*>(ts.lce1 + c * 6);
-      const double2 l01 = lc2[0], l23 = lc2[1], l45 = lc2[2];
-      const double lcr[8] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y, 0.0, 0.0};
-#elif EIK_LCE1
       const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const double2 l01 = ldv2_nc(lce1 + (int64_t)c * 6), l23 = ldv2_nc(lce1 + (int64_t)c * 6 + 2),
-                    l45 = ldv2_nc(lce1 + (int64_t)c * 6 + 4);
-      const double lcr[8] = {l01.x, l01.y, l23.x, l23.y, l45.x, l45.y, 0.0, 0.0};
-#else
-      const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const double4 l03 = ldv_nc(reinterpret_cast<const double4*>(S.Lc + i * 8));
-      const double2 l45 = ldv2_nc(S.Lc + i * 8 + 4);
-      const double lcr[8] = {l03.x, l03.y, l03.z, l03.w, l45.x, l45.y, 0.0, 0.0};
-#endif
-#if EIK_PRE3
-      const JvOwn o = jv_own(S, ai, Ui, lai);
-      JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      jv_accum<PCH>(S, ts, row.s, lcr, 0, pre, o, a);
-#pragma unroll
-      for (int k0 = PCH; k0 < KCMAX; k0 += PCH) {
-        CoefChunk<PCH> cf;
-        coef_load<PCH>(S, i, k0, cf);
-        asm volatile("" ::: "memory");
-        jv_accum<PCH>(S, ts, row.s, lcr, k0, cf, o, a);
-      }
-#elif EIK_PIPE3
-      // software-pipelined coefficient stream: chunk k+1's loads are issued
-      // before chunk k's math, so a thread always has a chunk in flight
-      constexpr int PC = EIK_PIPE3;
-      const JvOwn o = jv_own(S, ai, Ui, lai);
-      JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      CoefChunk<PC> cA, cB;
-      coef_load<PC>(S, i, 0, cA);
-#pragma unroll
-      for (int k0 = 0; k0 < KCMAX; k0 += 2 * PC) {
-        if (k0 + PC < KCMAX) coef_load<PC>(S, i, k0 + PC, cB);
-        asm volatile("" ::: "memory");
-        jv_accum<PC>(S, ts, row.s, lcr, k0, cA, o, a);
-        if (k0 + PC < KCMAX) {
-          if (k0 + 2 * PC < KCMAX) coef_load<PC>(S, i, k0 + 2 * PC, cA);
-          asm volatile("" ::: "memory");
-          jv_accum<PC>(S, ts, row.s, lcr, k0 + PC, cB, o, a);
-        }
-      }
-#else
-      const JvAcc a = swe_jv_part<0, KCMAX>(S, ts, row.s, lcr, 0, c, i, ai, Ui, lai);
-#endif
-#if EIK_CPA
-      const double4 z = S.scale * swe_jv_finish(S, a, ts.neb[c], ai, Ui);
-#else
+      const Lrow lr = load_lrow(lce1 + (int64_t)c * 6);
+      const JvAcc a = swe_jv_sum(S, ts, row.s, lr.v, i, ai, Ui, lai);
       const double4 z = S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
-#endif
-#if EIK_VMB
-      const double4 vm = F.epi_vm1 ? ts.vmb[c] : d4(0.0);
-#else
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
-#endif
       epi(i, z, ai, vm);
     }
     __syncthreads();
@@ -1475,24 +677,6 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
   }
 #endif
 #undef SRP_MARK
-}
-
-__device__ __forceinline__ void tile_prefetch_l2(const SweOp& S, int t) {
-  const int64_t c0 = __ldg(S.t_cell0 + t);
-  const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t);
-  if (nT <= 0) return;
-  const char* base0 = reinterpret_cast<const char*>(S.coefc + c0);
-  const int64_t lo = (int64_t)(reinterpret_cast<uintptr_t>(base0) & 127);
-  const int lines = (int)((lo + (int64_t)nT * 8 + 127) >> 7);
-  const char* aligned = base0 - lo;
-  const int tot = NCOEF * lines;
-  for (int q = threadIdx.x; q < tot; q += TPB) {
-    const int r = q / lines, l = q - r * lines;
-    pf_l2(aligned + (int64_t)r * S.NC * 8 + (int64_t)l * 128);
-  }
-  const char* lb = reinterpret_cast<const char*>(S.LcE1 + (int64_t)__ldg(S.t_e1off + t) * 6);
-  const int ll = (nE1 * 48 + 127) >> 7;
-  for (int q = threadIdx.x; q < ll; q += TPB) pf_l2(lb + (int64_t)q * 128);
 }
 
 struct SrcPtr {
