@@ -748,6 +748,9 @@ __host__ __device__ constexpr int dense_ld(int n) { return ((n + 3) & ~3) + 1; }
 struct DenseRed {
   double red[32];
   int ival;
+  int piv[kDenseCap];     // blk_solve: pivot row of each elimination step
+  double dg[kDenseCap];   // blk_solve: pivot values
+  double rinv[kDenseCap]; // blk_solve: their reciprocals
 };
 
 // C = A B; C must not alias A or B.  Thread -> 4 x 4 output block
@@ -808,65 +811,90 @@ __device__ double blk_norm1(DenseRed& rs, const double* M, int n, int ld) {
   return r;
 }
 
-// Solve P X = Q in place (Q <- X), P overwritten by its LU factors.
+// Solve P X = Q (Q <- X; P is destroyed): Gauss-Jordan elimination with
+// partial pivoting (first index of max |P[r][k]| among the rows not yet
+// pivoted, like LAPACK's idamax) done in place with implicit row
+// interchanges, so an elimination step is one barrier: every warp finds the
+// pivot redundantly, then eliminates column k from its own rows (pivot row
+// read-only in that step).  Equivalent to dgesv's LU + substitution up to
+// rounding.  The reference calls np.linalg.solve(V - U, V + U)
+// (kernels.py:142).
 template <int NT>
 __device__ void blk_solve(DenseRed& rs, double* P, double* Q, int n, int ld) {
+  const int lane = threadIdx.x & 31;
+  unsigned used = 0u;  // warp 0, bit q: row lane + 32 q is a pivot row already
   for (int k = 0; k < n; ++k) {
-    // pivot: first index of max |P[i][k]|, i >= k (warp 0)
+    // pivot (warp 0): |P[r][k]| compared as IEEE bit patterns (monotonic for
+    // x >= 0), reduced with three 32-bit warp reductions (hi, lo, row)
     if (threadIdx.x < 32) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + threadIdx.x; i < n; i += 32) {
-        const double v = fabs(P[(int64_t)i * ld + k]);
-        if (v > best) { best = v; bi = i; }
+      unsigned long long key = 0ull;
+      int bi = n;
+      for (int q = 0; lane + 32 * q < n; ++q) {
+        const int r = lane + 32 * q;
+        if ((used >> q) & 1u) continue;
+        const unsigned long long b =
+            (unsigned long long)__double_as_longlong(fabs(P[(int64_t)r * ld + k]));
+        if (bi == n || b > key) { key = b; bi = r; }
       }
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned hmax = __reduce_max_sync(0xffffffffu, bi < n ? hi : 0u);
+      const unsigned lmax = __reduce_max_sync(0xffffffffu, (bi < n && hi == hmax) ? lo : 0u);
+      const bool cand = bi < n && hi == hmax && lo == lmax;
+      const int pw = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)bi : 0xffffffffu);
+      if ((pw & 31) == lane) used |= 1u << (pw >> 5);
+      if (lane == 0) {
+        const double pk = P[(int64_t)pw * ld + k];
+        rs.piv[k] = pw;
+        rs.dg[k] = pk;
+        rs.rinv[k] = 1.0 / pk;
+      }
+    }
+    __syncthreads();
+    const int p = rs.piv[k];
+    // eliminate column k from every other row: thread -> (column lane of a
+    // 128-wide chunk, row group); P columns k+1 .. n-1 then Q columns
+    // 0 .. n-1.  The pivot row and column k are only read in this step.
+    constexpr int CW = 128, RG = NT / CW;
+    static_assert(NT % CW == 0, "blk_solve: NT multiple of 128");
+    const double rinv = rs.rinv[k];
+    const int np = n - k - 1;
+    const int nc = np + n;
+    const int cl = threadIdx.x % CW, g = threadIdx.x / CW;
+    for (int cb = 0; cb < nc; cb += CW) {
+      const int c = cb + cl;
+      if (c < nc) {
+        double* col = c < np ? P + (k + 1 + c) : Q + (c - np);
+        const double pv = col[(int64_t)p * ld];
+        for (int r0 = g; r0 < n; r0 += 4 * RG) {
+          double lv[4], v[4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          for (int q = 0; q < 4; ++q) {
+            const int r = r0 + q * RG;
+            const bool ok = r < n && r != p;
+            lv[q] = ok ? P[(int64_t)r * ld + k] : 0.0;
+            v[q] = ok ? col[(int64_t)r * ld] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = r0 + q * RG;
+            if (r < n && r != p) col[(int64_t)r * ld] = v[q] - (lv[q] * rinv) * pv;
+          }
+        }
       }
-      if (threadIdx.x == 0) rs.ival = bi;
-    }
-    __syncthreads();
-    const int piv = rs.ival;
-    if (piv != k) {
-      for (int j = threadIdx.x; j < n; j += NT) {
-        double t = P[(int64_t)k * ld + j];
-        P[(int64_t)k * ld + j] = P[(int64_t)piv * ld + j];
-        P[(int64_t)piv * ld + j] = t;
-        t = Q[(int64_t)k * ld + j];
-        Q[(int64_t)k * ld + j] = Q[(int64_t)piv * ld + j];
-        Q[(int64_t)piv * ld + j] = t;
-      }
-      __syncthreads();
-    }
-    const double rinv = 1.0 / P[(int64_t)k * ld + k];
-    for (int i = k + 1 + threadIdx.x; i < n; i += NT) P[(int64_t)i * ld + k] *= rinv;
-    __syncthreads();
-    // trailing update of P and Q: warp -> row, lane -> column
-    const int w0 = k + 1 - (k + 1) % 32;  // P columns from a 32-aligned start
-    for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
-      const double l = P[(int64_t)i * ld + k];
-      for (int j = w0 + (int)(threadIdx.x & 31); j < n; j += 32)
-        if (j > k) P[(int64_t)i * ld + j] -= l * P[(int64_t)k * ld + j];
-      for (int j = threadIdx.x & 31; j < n; j += 32)
-        Q[(int64_t)i * ld + j] -= l * Q[(int64_t)k * ld + j];
     }
     __syncthreads();
   }
-  // back substitution (dtrsm upper, non-unit)
-  for (int k = n - 1; k >= 0; --k) {
-    const double pkk = P[(int64_t)k * ld + k];
-    for (int j = threadIdx.x; j < n; j += NT) Q[(int64_t)k * ld + j] /= pkk;
-    __syncthreads();
-    for (int i = (int)(threadIdx.x >> 5); i < k; i += NT / 32) {
-      const double pik = P[(int64_t)i * ld + k];
-      for (int j = threadIdx.x & 31; j < n; j += 32)
-        Q[(int64_t)i * ld + j] -= Q[(int64_t)k * ld + j] * pik;
-    }
-    __syncthreads();
+  // X[k] = Q[piv[k]] / pivot_k, staged through P's storage
+  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+    const int k = idx / n, j = idx - k * n;
+    P[(int64_t)k * ld + j] = Q[(int64_t)rs.piv[k] * ld + j] / rs.dg[k];
   }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+    const int k = idx / n, j = idx - k * n;
+    Q[(int64_t)k * ld + j] = P[(int64_t)k * ld + j];
+  }
+  __syncthreads();
 }
 
 // exp(M[0]) for the n x n matrix in M[0] (six matrices of n x ld scratch);
@@ -1006,7 +1034,7 @@ __device__ void dense_phi(DenseRed& rs, const EngineWork& Wk, double* buf, int64
 }
 
 // shared-memory budget of the dedicated dense kernel
-constexpr int kDenseNT = 1024;
+constexpr int kDenseNT = 256;
 constexpr size_t kDenseKernelSmem = 220 * 1024;
 __host__ __device__ constexpr bool dense_fits_smem(int dim) {
   return (size_t)6 * dim * dense_ld(dim) * 8 <= kDenseKernelSmem;
