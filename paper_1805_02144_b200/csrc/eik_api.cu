@@ -135,6 +135,22 @@ template <class Epi>
 __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
                          const double4* U, const double4* fn, Epi epi,
                          double* part) {
+  if (S.tiled_ok) {
+    // two tiled passes over the same tiles (each own cell stays with its
+    // thread, so no barrier between them): F(U) - f_n into lapA, then
+    // subtract J (U - u_n) with x = (U - 1 * u_n) / 1 formed on the halo
+    double r[1] = {0.0};
+    double4* dtmp = S.lapA;
+    Form FA{U, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+    swe_tiled_op(sm, S, FA, RhsStep{}, [&](int64_t i, double4 F, double4 w, double4) {
+      dtmp[i] = F - fn[i];
+      r[0] += nf4(F) + nf4(w);
+    });
+    Form FB{U, nullptr, S.lin, 0.0, 1.0, 1.0, nullptr, nullptr};
+    swe_tiled(sm, S, FB, [&](int64_t i, double4 z, double4, double4) { epi(i, dtmp[i] - z); });
+    grid_reduce<1>(grid, sm, r, part);
+    return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
+  }
   int64_t lo, hi;
   brange(S.N, lo, hi);
   SrcPtr su{U};

@@ -556,6 +556,79 @@ __device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a,
   return r;
 }
 
+// Step-3 operators of the tiled pass (own cell i, its staged values ai,
+// Ui (the E1 stage) and lai = (L x)_i):
+//   JvStep:  z = scale * (J x)_i, E1 stage = linearisation state U;
+//   RhsStep: F(w)_i (swe.py:149-168) on the compact stencil, w staged as x,
+//            E1 stage = (h_s, 0, 0, 0).
+struct JvStep {
+  static constexpr bool kStageHs = false;
+  __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
+                                                const short* row, const double* lc, int64_t i,
+                                                double4 ai, double4 Ui, double4 lai) const {
+    const JvAcc a = swe_jv_sum(S, ts, row, lc, i, ai, Ui, lai);
+    return S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
+  }
+};
+
+template <int CH>
+__device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, const short* row,
+                                          const double* lc, int s0, const CoefChunk<CH>& cf,
+                                          double4 wi, double Ei, double4 lai, JvAcc& a) {
+  const double fxi = wi.x * wi.w, fyi = wi.y * wi.w, fzi = wi.z * wi.w;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int s = s0 + k;
+    const int l = row[s];
+    const double vx = cf.v[k][0], vy = cf.v[k][1], vz = cf.v[k][2];
+    const double gcx = cf.v[k][3], gcy = cf.v[k][4], gcz = cf.v[k][5];
+    const double dx = cf.v[k][6], dy = cf.v[k][7], dz = cf.v[k][8];
+    const double l0 = lc[s];
+    const double4 wj = sld(ts.x, l);
+    const double hsj = sld(ts.U, l).x;
+    const double4 la = sld(ts.La, l);
+    a.zeta += vx * (wj.x - wi.x) + vy * (wj.y - wi.y) + vz * (wj.z - wi.z);
+    const double Ej = 0.5 * (wj.x * wj.x + wj.y * wj.y + wj.z * wj.z) + S.g * (wj.w + hsj);
+    a.gx += gcx * (Ej - Ei);
+    a.gy += gcy * (Ej - Ei);
+    a.gz += gcz * (Ej - Ei);
+    a.dv += dx * (wj.x * wj.w + fxi) + dy * (wj.y * wj.w + fyi) + dz * (wj.z * wj.w + fzi);
+    a.l0 += l0 * (la.x - lai.x);
+    a.l1 += l0 * (la.y - lai.y);
+    a.l2 += l0 * (la.z - lai.z);
+    a.l3 += l0 * (la.w - lai.w);
+  }
+}
+
+struct RhsStep {
+  static constexpr bool kStageHs = true;
+  __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
+                                                const short* row, const double* lc, int64_t i,
+                                                double4 wi, double4 hsi4, double4 lai) const {
+    const double Ei = 0.5 * (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * (wi.w + hsi4.x);
+    JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    constexpr int CH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
+#pragma unroll
+    for (int k0 = 0; k0 < KCMAX; k0 += CH) {
+      CoefChunk<CH> cf;
+      coef_load<CH>(S, i, k0, cf);
+      asm volatile("" ::: "memory");
+      rhs_accum<CH>(S, ts, row, lc, k0, cf, wi, Ei, lai, a);
+    }
+    const double4 q = S.nf[i];
+    const double eta = a.zeta + q.w;
+    const double px = q.y * wi.z - q.z * wi.y;
+    const double py = q.z * wi.x - q.x * wi.z;
+    const double pz = q.x * wi.y - q.y * wi.x;
+    double4 r;
+    r.x = -eta * px - a.gx - S.nu * a.l0;
+    r.y = -eta * py - a.gy - S.nu * a.l1;
+    r.z = -eta * pz - a.gz - S.nu * a.l2;
+    r.w = -a.dv - S.nu * a.l3;
+    return r;
+  }
+};
+
 // How a tiled pass builds its input vector on the fly at every E2 cell:
 //   x = ((src - a1 * vm2) - a2 * vm1) / h     (vm2 / vm1 optional)
 // i.e. the MGS update and normalisation of krylov.py:91-104 fused into the
@@ -581,8 +654,9 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
 // the own cells -> epi(i, z, x_i, epi_vm1_i).  A whole Krylov iteration
 // (orthogonalise + normalise v_j, L v_j, J v_j, projections) is one such
 // pass: one HBM sweep and one grid barrier per iteration.
-template <class Epi>
-__device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& epi) {
+template <class Step, class Epi>
+__device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step& step,
+                             const Epi& epi) {
   const TileSmem ts = tile_smem(S);
 #if EIK_PROF
   long long pst[3] = {0, 0, 0}, pt = clock64();
@@ -610,13 +684,17 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
         a0 = ldv(F.src + ga);
         if (F.vm2) a1 = ldv(F.vm2 + ga);
         if (F.vm1) a2 = ldv(F.vm1 + ga);
-        if (ca < nE1) ua = ldv_nc(S.lin + ga);
+        if (ca < nE1)
+          ua = Step::kStageHs ? make_double4(__ldg(S.hs + ga), 0.0, 0.0, 0.0)
+                                : ldv_nc(S.lin + ga);
       }
       if (vb) {
         b0 = ldv(F.src + gb);
         if (F.vm2) b1 = ldv(F.vm2 + gb);
         if (F.vm1) b2 = ldv(F.vm1 + gb);
-        if (cb < nE1) ub = ldv_nc(S.lin + gb);
+        if (cb < nE1)
+          ub = Step::kStageHs ? make_double4(__ldg(S.hs + gb), 0.0, 0.0, 0.0)
+                                : ldv_nc(S.lin + gb);
       }
       if (va) {
         const double4 x = form_x(F, a0, a1, a2);
@@ -662,8 +740,7 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
       const double4 lai = sld(ts.La, c);
       const Row8 row = load_row8(rows + (int64_t)c * 8);
       const Lrow lr = load_lrow(lce1 + (int64_t)c * 6);
-      const JvAcc a = swe_jv_sum(S, ts, row.s, lr.v, i, ai, Ui, lai);
-      const double4 z = S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
+      const double4 z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
     }
@@ -677,6 +754,12 @@ __device__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F, const Epi& ep
   }
 #endif
 #undef SRP_MARK
+}
+
+template <class Epi>
+__device__ __forceinline__ void swe_tiled(Smem& sm, const SweOp& S, const Form& F,
+                                          const Epi& epi) {
+  swe_tiled_op(sm, S, F, JvStep{}, epi);
 }
 
 struct SrcPtr {

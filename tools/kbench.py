@@ -7,7 +7,10 @@ from paper_1805_02144_b200 import swe as gswe, _native as nat
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-ops, u0, spec = make_config(name)
+lvl = None
+if ":" in name:
+    name, lvl = name.split(":")
+ops, u0, spec = make_config(name, level=lvl)
 ctx = gswe.SweContext(ops)
 info = (C.c_int64 * 14)()
 nat.check(nat.load().eik_swe_info(ctx.h, info))
