@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--scheme", default="exprb42")
+    ap.add_argument("--level", type=int, default=None, help="grid level override (C4: 9 or 10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sweep-steps", type=int, default=5)
@@ -160,7 +161,7 @@ def run_reference(args):
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = str(threads)
     from paper_1805_02144_b200.states import make_config
-    ops, u0, spec = make_config(args.config)
+    ops, u0, spec = make_config(args.config, level=args.level)
     spec.scheme = args.scheme
     nsteps = max(1, min(args.steps, 2))
     secs = cpu_baseline_oracle(ops, u0, spec, nsteps)
@@ -200,7 +201,7 @@ def main():
     from paper_1805_02144_b200 import swe as gswe
     from paper_1805_02144_b200.states import make_config
 
-    ops, u0, spec = make_config(args.config)
+    ops, u0, spec = make_config(args.config, level=args.level)
     scheme = args.scheme
     ctx = gswe.SweContext(ops, device=local)
     ctx.set_state(u0)
