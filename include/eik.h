@@ -104,6 +104,17 @@ typedef struct {
 const char* eik_last_error(void);
 int eik_version(void);
 
+/* Device cell order used by eik_swe_create (host only, no GPU needed):
+ * recursive coordinate bisection of the n cell positions (px, py, pz) into
+ * ntiles leaves whose sizes differ by at most one (median split along the
+ * longest extent, ties by index; constant positions keep the index order).
+ * ord[d] = original index of device cell d (n entries), starts[t] = first
+ * device cell of leaf t (ntiles + 1 entries, starts[ntiles] = n).  Each leaf
+ * is one tile of the Krylov pass.  No reference counterpart: the reference
+ * has no device layout (its cell order is the grid's, swe.py:23-46). */
+eik_status eik_tile_order(int64_t n, const double* px, const double* py, const double* pz,
+                          int32_t ntiles, int32_t* ord, int32_t* starts);
+
 /* ---------------------------------------------------------------- SWE */
 /* ops[11] = Gx Gy Gz Dx Dy Dz Vx Vy Vz L Df (each n_g x n_g CSR).  The
  * device path applies Df as -nu * L(L .); the creation checks that the

@@ -55,6 +55,8 @@ _D = C.POINTER(C.c_double)
 _SIGS = {
     "eik_last_error": (C.c_char_p, []),
     "eik_version": (C.c_int, []),
+    "eik_tile_order": (C.c_int, [C.c_int64, _D, _D, _D, C.c_int32, C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32)]),
     "eik_swe_create": (C.c_int, [C.c_int32, C.POINTER(EikCsrView), _D, _D, _D,
                                  _D, _D, C.c_double, C.c_double, C.c_int32,
                                  C.c_int32, C.POINTER(_P)]),

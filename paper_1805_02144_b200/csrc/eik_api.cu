@@ -1038,6 +1038,18 @@ extern "C" {
 const char* eik_last_error(void) { return g_err.c_str(); }
 int eik_version(void) { return 1; }
 
+eik_status eik_tile_order(int64_t n, const double* px, const double* py, const double* pz,
+                          int32_t ntiles, int32_t* ord, int32_t* starts) {
+  if (n < 1 || n > INT32_MAX || ntiles < 1 || !px || !py || !pz || !ord || !starts)
+    return fail(EIK_EINVAL, "invalid arguments to eik_tile_order");
+  std::vector<int32_t> st;
+  for (int64_t i = 0; i < n; ++i) ord[i] = (int32_t)i;
+  rcb_order(px, py, pz, ord, 0, n, ntiles, st);
+  st.push_back((int32_t)n);
+  for (size_t t = 0; t < st.size(); ++t) starts[t] = st[t];
+  return EIK_OK;
+}
+
 eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
                           const double* n_y, const double* n_z, const double* f,
                           const double* h_s, double g, double nu, int32_t device,
