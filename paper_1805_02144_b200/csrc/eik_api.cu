@@ -130,6 +130,23 @@ __device__ int phase_rhs(cg::grid_group& grid, Smem& sm, const SweOp& S,
   return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
 }
 
+// F(u_n), eta and v_1 = dt F(u_n) at the start of a step: one tiled pass on
+// the compact stencil when it is valid (the API-level F keeps the CSR-order
+// phase_rhs, which reproduces scipy's csr_matvec order)
+__device__ int phase_rhs_step(cg::grid_group& grid, Smem& sm, const SweOp& S, const double4* u,
+                              double4* out_f, double4* out_v, double dt, double* part) {
+  if (!S.tiled_ok) return phase_rhs(grid, sm, S, u, out_f, out_v, dt, true, part);
+  double r[1] = {0.0};
+  Form FA{u, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+  swe_tiled_op(sm, S, FA, RhsStep{true}, [&](int64_t i, double4 F, double4 w, double4) {
+    out_f[i] = F;
+    out_v[i] = dt * F;
+    r[0] += nf4(F) + nf4(w);
+  });
+  grid_reduce<1>(grid, sm, r, part);
+  return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
+}
+
 // d = (F(U) - f_n) - J (U - u_n)   (integrators.py:101-102), epilogue(i, d)
 template <class Epi>
 __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
@@ -142,7 +159,7 @@ __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
     double r[1] = {0.0};
     double4* dtmp = S.lapA;
     Form FA{U, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
-    swe_tiled_op(sm, S, FA, RhsStep{}, [&](int64_t i, double4 F, double4 w, double4) {
+    swe_tiled_op(sm, S, FA, RhsStep{false}, [&](int64_t i, double4 F, double4 w, double4) {
       dtmp[i] = F - fn[i];
       r[0] += nf4(F) + nf4(w);
     });
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_step(SweArgs A) {
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
   ProfClock pc;
-  int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, true, A.Wk.part);
+  int st = phase_rhs_step(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, A.Wk.part);
   pc.mark(PC_RHS);
   if (st != EIK_OK) { set_status(A.status, st); return; }
   // loop state in local memory: none of it may hold registers across sweeps
@@ -456,7 +473,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
   volatile int in_engine;
   StepState* G = A.ss;
   if (!A.resume) {
-    const int st = phase_rhs(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, true, A.Wk.part);
+    const int st = phase_rhs_step(grid, sm, A.S1, A.u, A.fn, A.v1, A.dt, A.Wk.part);
     pc.mark(PC_RHS);
     if (st != EIK_OK) { cont_stop(A, st); return; }
     nA = (int64_t)phase_count_nnz(grid, sm, A.S1, A.Wk.part);

@@ -602,6 +602,7 @@ __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, co
 
 struct RhsStep {
   static constexpr bool kStageHs = true;
+  bool write_ne;  // store (n, eta) of every own cell to S.ne (linearisation at w)
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
                                                 double4 wi, double4 hsi4, double4 lai) const {
@@ -617,6 +618,7 @@ struct RhsStep {
     }
     const double4 q = S.nf[i];
     const double eta = a.zeta + q.w;
+    if (write_ne) S.ne[i] = make_double4(q.x, q.y, q.z, eta);
     const double px = q.y * wi.z - q.z * wi.y;
     const double py = q.z * wi.x - q.x * wi.z;
     const double pz = q.x * wi.y - q.y * wi.x;
