@@ -163,7 +163,7 @@ __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
       dtmp[i] = F - fn[i];
       r[0] += nf4(F) + nf4(w);
     });
-    Form FB{U, nullptr, S.lin, 0.0, 1.0, 1.0, nullptr, nullptr};
+    Form FB{U, nullptr, S.lin, 0.0, 1.0, 1.0, nullptr, nullptr, 1};  // reversed: L2 reuse
     swe_tiled(sm, S, FB, [&](int64_t i, double4 z, double4, double4) { epi(i, dtmp[i] - z); });
     grid_reduce<1>(grid, sm, r, part);
     return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;

@@ -123,6 +123,36 @@ __device__ __forceinline__ void stv(double4* p, double4 v) {
                : "memory");
 }
 
+// L2 residency hints (EIK_L2POL): the Krylov vectors written by a pass are
+// stored evict_last (read again in the next iteration, first by the tiles
+// that wrote them last, see Form::rev); the coefficient stream is loaded
+// evict_first.
+#ifndef EIK_L2POL
+#define EIK_L2POL 1
+#endif
+
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void stv_pol(double4* p, double4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v.x),
+               "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ double ld_stream_pol(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // ---------------------------------------------------------------- shared
 struct Smem {
   double red[NWARP][NPART];
@@ -470,7 +500,13 @@ __device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, Coe
   for (int k = 0; k < CH; ++k) {
     const double* cp = S.coefc + i + (s0 + k) * st;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) cf.v[k][q] = __ldcs(cp + q * S.NC);
+    for (int q = 0; q < 9; ++q) {
+#if EIK_L2POL
+      cf.v[k][q] = ld_stream_pol(cp + q * S.NC, pol_evict_first());
+#else
+      cf.v[k][q] = __ldcs(cp + q * S.NC);
+#endif
+    }
   }
 }
 // own-cell terms shared by every slot
@@ -642,7 +678,11 @@ struct Form {
   double a1, a2, h;
   double4* out;
   const double4* epi_vm1;  // own-cell vector handed to the epilogue (may be null)
+  int rev = 0;             // walk the CTA's tiles in reverse order
 };
+#ifndef EIK_REV
+#define EIK_REV 1
+#endif
 
 __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
                                           double4 s2) {
@@ -666,7 +706,12 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
 #else
 #define SRP_MARK(k)
 #endif
-  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+  // this CTA's tiles are t = blockIdx.x + k * gridDim.x; F.rev walks them
+  // backwards (alternate Krylov iterations: the tiles written last in one
+  // iteration are read first in the next, while their vectors are in L2)
+  const int kt = S.ntiles > (int)blockIdx.x ? (S.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  for (int k = 0; k < kt; ++k) {
+    const int t = (int)blockIdx.x + (EIK_REV && F.rev ? kt - 1 - k : k) * (int)gridDim.x;
     const int64_t c0 = __ldg(S.t_cell0 + t);
     const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
     if (nT == 0) continue;  // uniform over the CTA
@@ -702,13 +747,19 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
         const double4 x = form_x(F, a0, a1, a2);
         sst(ts.x, ca, x);
         if (ca < nE1) sst(ts.U, ca, ua);
-        if (F.out && ca < nT) stv(F.out + ga, x);
+        if (F.out && ca < nT) {
+          if (EIK_L2POL) stv_pol(F.out + ga, x, pol_evict_last());
+          else stv(F.out + ga, x);
+        }
       }
       if (vb) {
         const double4 x = form_x(F, b0, b1, b2);
         sst(ts.x, cb, x);
         if (cb < nE1) sst(ts.U, cb, ub);
-        if (F.out && cb < nT) stv(F.out + gb, x);
+        if (F.out && cb < nT) {
+          if (EIK_L2POL) stv_pol(F.out + gb, x, pol_evict_last());
+          else stv(F.out + gb, x);
+        }
       }
     }
     __syncthreads();
@@ -1180,10 +1231,12 @@ __device__ KrylovState krylov_tiled(cg::grid_group& grid, Smem& sm, const SweOp&
           F.h = hc;
           F.out = vj;
           F.epi_vm1 = vm1;
+          F.rev = (int)(j & 1);
           swe_tiled(
               sm, op, F,
               [&](int64_t i, double4 z, double4 x, double4 b) {
-                stv(zout + i, z);
+                if (EIK_L2POL) stv_pol(zout + i, z, pol_evict_last());
+                else stv(zout + i, z);
                 d[1] += dot4(x, z);
                 d[3] += dot4(z, z);
                 d[4] += dot4(x, x);
