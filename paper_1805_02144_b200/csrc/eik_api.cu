@@ -834,7 +834,7 @@ struct EngineHost {
     CK(mem.get(&wk.ybuf[0], NU));
     CK(mem.get(&wk.ybuf[1], NU));
     CK(mem.get(&wk.zero, NU));
-    CK(mem.get(&wk.part, (size_t)2 * G * NPART));
+    CK(mem.get(&wk.part, (size_t)2 * NPART * part_stride(G)));
     CK(mem.get(&wk.H, (size_t)m_alloc * m_alloc));
     CK(mem.get(&wk.scr, (size_t)6 * MAXDIM * MAXDIM));
     CK(mem.get(&wk.phi, MAXDIM + 4));

@@ -175,66 +175,55 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// CTA partial -> part[blockIdx.x][0..NV)
-template <int NV>
-__device__ void part_store(Smem& sm, double (&v)[NV], double* part) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = warp_sum(v[k]);
-    if (lane == 0) sm.red[w][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < NWARP; ++q) s += sm.red[q][threadIdx.x];
-    part[(int64_t)blockIdx.x * NPART + threadIdx.x] = s;
-  }
-  __syncthreads();
-}
-
-// after grid.sync(): identical totals in every CTA
-template <int NV>
-__device__ void part_total(Smem& sm, const double* part, double (&out)[NV]) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double v[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += TPB) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] += __ldcg(part + (int64_t)b * NPART + k);
-  }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = warp_sum(v[k]);
-    if (lane == 0) sm.red[w][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < NWARP; ++q) s += sm.red[q][threadIdx.x];
-    sm.tot[threadIdx.x] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) out[k] = sm.tot[k];
-  __syncthreads();
-}
-
+// Deterministic grid-wide sums: every CTA writes its partials, value-major
+// (part[k][b], k < NV, rows padded to a multiple of 32 CTAs), and after the
+// grid barrier every CTA reduces them in the same fixed order -- warp k sums
+// value k with coalesced loads -- so all CTAs hold bit-identical totals.
 // Partials are double-buffered: a fast CTA may start the next reduction's
-// part_store while a slow CTA still reads this one's partials; the two
-// buffers alternate, and at least one grid.sync separates reuse.
+// store while a slow CTA still reads this one's; the two buffers alternate
+// and at least one grid.sync separates reuse.  `part` holds 2 * NPART * Gp
+// doubles, Gp = gridDim.x rounded up to 32.
+__host__ __device__ constexpr int part_stride(int G) { return (G + 31) & ~31; }
+
 template <int NV>
-__device__ void grid_reduce(cg::grid_group& grid, Smem& sm, double (&v)[NV],
-                            double* part) {
+__device__ void grid_reduce(cg::grid_group& grid, Smem& sm, double (&v)[NV], double* part) {
+  static_assert(NV <= NWARP && NV <= NPART, "one warp per reduced value");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int G = gridDim.x, Gp = part_stride(G);
   const int par = sm.par;
-  double* P = part + (int64_t)par * gridDim.x * NPART;
-  part_store<NV>(sm, v, P);
+  double* P = part + (int64_t)par * NPART * Gp;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double s = warp_sum(v[k]);
+    if (lane == 0) sm.red[w][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < NWARP; ++q) s += sm.red[q][threadIdx.x];
+    __stcg(P + (int64_t)threadIdx.x * Gp + blockIdx.x, s);
+  }
   if (threadIdx.x == 0) sm.par = par ^ 1;
   grid.sync();
-  part_total<NV>(sm, P, v);
+  if (w < NV) {
+    const double* row = P + (int64_t)w * Gp;
+    double s = 0.0;
+    for (int b0 = 0; b0 < G; b0 += 32 * 8) {
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = b0 + lane + 32 * q;
+        x[q] = b < G ? __ldcg(row + b) : 0.0;
+      }
+      s += ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+    }
+    s = warp_sum(s);
+    if (lane == 0) sm.tot[w] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = sm.tot[k];
 }
 
 // =================================================================== operators
