@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--scheme", default="exprb42")
     ap.add_argument("--level", type=int, default=None, help="grid level override (C4: 9 or 10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="steps of the e2e replay (default: all timed steps)")
     ap.add_argument("--sweep-steps", type=int, default=5)
     return ap.parse_args()
 
@@ -214,8 +215,15 @@ def main():
         first = False
         return ctx.step(sch, spec.dt, spec.tol)
 
-    for _ in range(args.warmup):
+    from paper_1805_02144_b200 import _native as nat
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            u_prev_snap = ctx.get_state()
         step()
+    # snapshot of the trajectory at the start of the timed region (state,
+    # previous state, warm-start seeds): the e2e leg replays the same steps
+    u_snap = ctx.get_state()
+    seeds_snap = {slot: ctx.seeds(slot) for slot in nat.SLOT_IDS}
     torch.cuda.synchronize(local)
     if dist:
         dist.barrier()
@@ -242,17 +250,25 @@ def main():
     ms_per_step = ms / args.steps
 
     # end to end through the C ABI: pinned host state in, step, state out
-    # (two pinned buffers used in turn: step k's result is step k+1's input)
-    from paper_1805_02144_b200 import _native as nat
+    # -- the same first e2e_steps steps of the timed region, replayed from the
+    # snapshot; two pinned buffers used in turn (step k's result is step
+    # k+1's input)
     pins = [torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory() for _ in range(2)]
     bufs = [p.numpy() for p in pins]
-    bufs[0][:] = ctx.get_state()
+    bufs[0][:] = u_snap
+    if scheme == "epi3":
+        ctx.set_prev(u_prev_snap)
+    for slot, (tau, m) in seeds_snap.items():
+        ctx.set_seeds(slot, tau, m)
+    args.e2e_steps = args.steps if args.e2e_steps <= 0 else min(args.e2e_steps, args.steps)
     torch.cuda.synchronize(local)
+    e2e_dev_ms = 0.0
     te = time.perf_counter()
     for k in range(args.e2e_steps):
         hin, hout = bufs[k & 1], bufs[(k + 1) & 1]
         ctx.set_state(hin)
         step()
+        e2e_dev_ms += ctx.last_kernel_ms()
         nat.check(nat.load().eik_swe_get_state(ctx.h, nat.dptr(hout)), "get_state")
     e2e_wall = time.perf_counter() - te
     e2e, _ = aggregate_throughput(args.e2e_steps, 1e3 * e2e_wall, dist, f"cuda:{local}")
@@ -319,7 +335,9 @@ def main():
                              f"step_* = every J*v pass + candidate reads over the whole "
                              f"graph-replayed step; peak {src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * 4 * ops.n_g,
-                "d2h_bytes_per_step": 8 * 4 * ops.n_g},
+                "d2h_bytes_per_step": 8 * 4 * ops.n_g, "steps": args.e2e_steps,
+                "wall_ms_per_step": 1e3 * e2e_wall / args.e2e_steps,
+                "device_ms_per_step": e2e_dev_ms / args.e2e_steps},
         "gpu_launches": launches,
         "clocks": clocks,
     }
