@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0,
                     help="steps of the e2e replay (default: all timed steps)")
-    ap.add_argument("--sweep-steps", type=int, default=5)
+    ap.add_argument("--sweep-steps", type=int, default=0,
+                    help="timed steps replayed for the sweep roofline (default: all)")
     return ap.parse_args()
 
 
@@ -234,9 +235,11 @@ def main():
     dev_ms = 0.0
     mv = 0
     t0 = time.perf_counter()
+    step_ms = []
     for _ in range(args.steps):
         calls = step()
-        dev_ms += ctx.last_kernel_ms()
+        step_ms.append(ctx.last_kernel_ms())
+        dev_ms += step_ms[-1]
         mv += sum(int(c.matvecs) for c in calls)
     torch.cuda.synchronize(local)
     wall = time.perf_counter() - t0
@@ -253,13 +256,17 @@ def main():
     # -- the same first e2e_steps steps of the timed region, replayed from the
     # snapshot; two pinned buffers used in turn (step k's result is step
     # k+1's input)
+    def restore():
+        ctx.set_state(u_snap)
+        if scheme == "epi3":
+            ctx.set_prev(u_prev_snap)
+        for slot, (tau, m) in seeds_snap.items():
+            ctx.set_seeds(slot, tau, m)
+
     pins = [torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory() for _ in range(2)]
     bufs = [p.numpy() for p in pins]
     bufs[0][:] = u_snap
-    if scheme == "epi3":
-        ctx.set_prev(u_prev_snap)
-    for slot, (tau, m) in seeds_snap.items():
-        ctx.set_seeds(slot, tau, m)
+    restore()
     args.e2e_steps = args.steps if args.e2e_steps <= 0 else min(args.e2e_steps, args.steps)
     torch.cuda.synchronize(local)
     e2e_dev_ms = 0.0
@@ -273,13 +280,15 @@ def main():
     e2e_wall = time.perf_counter() - te
     e2e, _ = aggregate_throughput(args.e2e_steps, 1e3 * e2e_wall, dist, f"cuda:{local}")
 
-    # the dominant kernel alone: the same steps launched kernel by kernel
-    # (host-loop mode, identical results), every Krylov sweep kernel
-    # bracketed by CUDA events on the libeik stream
+    # the dominant kernel alone: the timed steps replayed from the snapshot,
+    # launched kernel by kernel (host-loop mode, identical results), every
+    # Krylov sweep kernel bracketed by CUDA events on the libeik stream
+    nsw_steps = args.steps if args.sweep_steps <= 0 else min(args.sweep_steps, args.steps)
+    restore()
     ctx.set_hostloop(True)
     ctx.sweep_timing(reset=True)
     k1 = ctx.krylov_iters()
-    for _ in range(max(1, min(args.steps, args.sweep_steps))):
+    for _ in range(nsw_steps):
         step()
     torch.cuda.synchronize(local)
     sweep_ms, nsweeps = ctx.sweep_timing(reset=True)
@@ -323,13 +332,13 @@ def main():
                      "kernel": "k_swe_sweep",
                      "launches": nsweeps, "iters_per_launch": iters_per_launch,
                      "us_per_iter": 1e3 * sweep_ms / max(sweep_iters, 1),
-                     "sweep_share_of_step": (sweep_ms / max(1, min(args.steps, args.sweep_steps))) / ms_per_step,
+                     "sweep_share_of_step": sweep_ms / sum(step_ms[:nsw_steps]),
                      "step_achieved": step_achieved, "step_frac": step_achieved / hbm,
                      "note": f"kernel = k_swe_sweep (one IOM2 Krylov sweep per launch, "
                              f"{iters_per_launch:.1f} iterations avg); achieved = B_alg "
                              f"{balg / 1e6:.1f} MB x iterations / CUDA-event time of the "
-                             f"sweep launches ({nsweeps} launches over "
-                             f"{max(1, min(args.steps, args.sweep_steps))} steps in host-loop "
+                             f"sweep launches ({nsweeps} launches over the "
+                             f"{nsw_steps} timed steps replayed in host-loop "
                              f"mode); traffic = ncu DRAM bytes per iteration of one captured "
                              f"launch (profiles/traffic.json) x iterations per launch; "
                              f"step_* = every J*v pass + candidate reads over the whole "
