@@ -138,7 +138,7 @@ __device__ int phase_rhs_step(cg::grid_group& grid, Smem& sm, const SweOp& S, co
   if (!S.tiled_ok) return phase_rhs(grid, sm, S, u, out_f, out_v, dt, true, part);
   double r[1] = {0.0};
   Form FA{u, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
-  swe_tiled_op(sm, S, FA, RhsStep{true}, [&](int64_t i, double4 F, double4 w, double4) {
+  swe_tiled_op(sm, S, FA, RhsStep{true, true}, [&](int64_t i, double4 F, double4 w, double4) {
     out_f[i] = F;
     out_v[i] = dt * F;
     r[0] += nf4(F) + nf4(w);
@@ -153,18 +153,13 @@ __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
                          const double4* U, const double4* fn, Epi epi,
                          double* part) {
   if (S.tiled_ok) {
-    // two tiled passes over the same tiles (each own cell stays with its
-    // thread, so no barrier between them): F(U) - f_n into lapA, then
-    // subtract J (U - u_n) with x = (U - 1 * u_n) / 1 formed on the halo
+    // one 1-ring tiled pass: [F*(U) - J*_n U] - g_n (DevStep)
     double r[1] = {0.0};
-    double4* dtmp = S.lapA;
-    Form FA{U, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
-    swe_tiled_op(sm, S, FA, RhsStep{false}, [&](int64_t i, double4 F, double4 w, double4) {
-      dtmp[i] = F - fn[i];
-      r[0] += nf4(F) + nf4(w);
+    Form FD{U, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+    swe_tiled_op(sm, S, FD, DevStep{}, [&](int64_t i, double4 d, double4 w, double4) {
+      epi(i, d);
+      r[0] += nf4(d) + nf4(w);
     });
-    Form FB{U, nullptr, S.lin, 0.0, 1.0, 1.0, nullptr, nullptr, 1};  // reversed: L2 reuse
-    swe_tiled(sm, S, FB, [&](int64_t i, double4 z, double4, double4) { epi(i, dtmp[i] - z); });
     grid_reduce<1>(grid, sm, r, part);
     return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
   }
@@ -1430,8 +1425,9 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(B.get(&c->ord_d, N));
   CKC(cudaMemcpy(c->ord_d, ord.data(), N * 4, cudaMemcpyHostToDevice));
   c->ord_h = ord;
-  double4 *ne, *lapA, *lapB;
+  double4 *ne, *lapA, *lapB, *gn;
   CKC(B.get(&ne, N));
+  CKC(B.get(&gn, N));
   CKC(B.get(&lapA, N));
   CKC(B.get(&lapB, N));
   CKC(cudaEventCreate(&c->ev0));
@@ -1452,6 +1448,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.ne = ne;
   S.lapA = lapA;
   S.lapB = lapB;
+  S.gn = gn;
   S.scale = 1.0;
   S.df1 = d_df1;
   S.dfx = d_dfx;

@@ -242,6 +242,7 @@ struct SweOp {
   double4* ne;           // (n_x, n_y, n_z, eta) at the linearisation state
   double4* lapA;         // scratch: L x
   double4* lapB;         // scratch: second L x
+  double4* gn;           // g_n = F*(u_n) - J* u_n (tiled D(U), see DevStep)
   double scale;          // A x = scale * (J x)   (integrators.py:117)
   // n_A counting data
   const double* df1;     // [K][N] Df(i, slot) (0 where Df has no entry)
@@ -588,6 +589,7 @@ __device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a,
 //            E1 stage = (h_s, 0, 0, 0).
 struct JvStep {
   static constexpr bool kStageHs = false;
+  static constexpr bool kE1Only = false;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
                                                 double4 ai, double4 Ui, double4 lai) const {
@@ -596,10 +598,17 @@ struct JvStep {
   }
 };
 
+// F on the compact stencil, with the G E sum split into its h_s-free part
+// (gx..) and the h_s part (hx..), and, for the step start, the J* sum of
+// J* u at u itself (jx..: e_j = u_j . u_j + g h_j).  * = without Df and h_s.
+struct RhsAcc {
+  double zeta, gx, gy, gz, hx, hy, hz, jx, jy, jz, dv, l0, l1, l2, l3;
+};
 template <int CH>
 __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, const short* row,
                                           const double* lc, int s0, const CoefChunk<CH>& cf,
-                                          double4 wi, double Ei, double4 lai, JvAcc& a) {
+                                          double4 wi, double Ei, double Hi, double Ji,
+                                          double4 lai, RhsAcc& a) {
   const double fxi = wi.x * wi.w, fyi = wi.y * wi.w, fzi = wi.z * wi.w;
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
@@ -613,10 +622,18 @@ __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, co
     const double hsj = sld(ts.U, l).x;
     const double4 la = sld(ts.La, l);
     a.zeta += vx * (wj.x - wi.x) + vy * (wj.y - wi.y) + vz * (wj.z - wi.z);
-    const double Ej = 0.5 * (wj.x * wj.x + wj.y * wj.y + wj.z * wj.z) + S.g * (wj.w + hsj);
+    const double Ej = 0.5 * (wj.x * wj.x + wj.y * wj.y + wj.z * wj.z) + S.g * wj.w;
     a.gx += gcx * (Ej - Ei);
     a.gy += gcy * (Ej - Ei);
     a.gz += gcz * (Ej - Ei);
+    const double Hj = S.g * hsj;
+    a.hx += gcx * (Hj - Hi);
+    a.hy += gcy * (Hj - Hi);
+    a.hz += gcz * (Hj - Hi);
+    const double Jj = (wj.x * wj.x + wj.y * wj.y + wj.z * wj.z) + S.g * wj.w;
+    a.jx += gcx * (Jj - Ji);
+    a.jy += gcy * (Jj - Ji);
+    a.jz += gcz * (Jj - Ji);
     a.dv += dx * (wj.x * wj.w + fxi) + dy * (wj.y * wj.w + fyi) + dz * (wj.z * wj.w + fzi);
     a.l0 += l0 * (la.x - lai.x);
     a.l1 += l0 * (la.y - lai.y);
@@ -627,19 +644,23 @@ __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, co
 
 struct RhsStep {
   static constexpr bool kStageHs = true;
+  static constexpr bool kE1Only = false;
   bool write_ne;  // store (n, eta) of every own cell to S.ne (linearisation at w)
+  bool write_gn;  // store g_n = F*(w) - J*(w) w to S.gn (for DevStep)
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
                                                 double4 wi, double4 hsi4, double4 lai) const {
-    const double Ei = 0.5 * (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * (wi.w + hsi4.x);
-    JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const double Ei = 0.5 * (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * wi.w;
+    const double Hi = S.g * hsi4.x;
+    const double Ji = (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * wi.w;
+    RhsAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     constexpr int CH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
 #pragma unroll
     for (int k0 = 0; k0 < KCMAX; k0 += CH) {
       CoefChunk<CH> cf;
       coef_load<CH>(S, i, k0, cf);
       asm volatile("" ::: "memory");
-      rhs_accum<CH>(S, ts, row, lc, k0, cf, wi, Ei, lai, a);
+      rhs_accum<CH>(S, ts, row, lc, k0, cf, wi, Ei, Hi, Ji, lai, a);
     }
     const double4 q = S.nf[i];
     const double eta = a.zeta + q.w;
@@ -647,12 +668,94 @@ struct RhsStep {
     const double px = q.y * wi.z - q.z * wi.y;
     const double py = q.z * wi.x - q.x * wi.z;
     const double pz = q.x * wi.y - q.y * wi.x;
+    if (write_gn) {
+      // F*(w) - J*(w) w, the same expression shapes as DevStep
+      double4 fs, js;
+      fs.x = -eta * px - a.gx;
+      fs.y = -eta * py - a.gy;
+      fs.z = -eta * pz - a.gz;
+      fs.w = -a.dv;
+      js.x = -(px * a.zeta) - eta * px - a.jx;
+      js.y = -(py * a.zeta) - eta * py - a.jy;
+      js.z = -(pz * a.zeta) - eta * pz - a.jz;
+      js.w = -(2.0 * a.dv);
+      S.gn[i] = fs - js;
+    }
     double4 r;
-    r.x = -eta * px - a.gx - S.nu * a.l0;
-    r.y = -eta * py - a.gy - S.nu * a.l1;
-    r.z = -eta * pz - a.gz - S.nu * a.l2;
+    r.x = -eta * px - (a.gx + a.hx) - S.nu * a.l0;
+    r.y = -eta * py - (a.gy + a.hy) - S.nu * a.l1;
+    r.z = -eta * pz - (a.gz + a.hz) - S.nu * a.l2;
     r.w = -a.dv - S.nu * a.l3;
     return r;
+  }
+};
+
+// D(U) = F(U) - f_n - J_n (U - u_n)  (integrators.py:101-102) in one 1-ring
+// pass: Df and the h_s term of F are linear in U and cancel exactly, and J is
+// linear, so D(U) = [F*(U) - J*_n U] - g_n with g_n = F*(u_n) - J*_n u_n
+// (RhsStep at the step start), * = without Df and h_s.  Staged: U as x and
+// the linearisation state u_n on E1; no Laplacian step.
+struct DevStep {
+  static constexpr bool kStageHs = false;
+  static constexpr bool kE1Only = true;
+  __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
+                                                const short* row, const double* /*lc*/,
+                                                int64_t i, double4 Ui, double4 li,
+                                                double4 /*lai*/) const {
+    const double Ei = 0.5 * (Ui.x * Ui.x + Ui.y * Ui.y + Ui.z * Ui.z) + S.g * Ui.w;
+    const double ei = li.x * Ui.x + li.y * Ui.y + li.z * Ui.z + S.g * Ui.w;
+    const double fxi = Ui.x * Ui.w, fyi = Ui.y * Ui.w, fzi = Ui.z * Ui.w;
+    const double kxi = li.w * Ui.x + li.x * Ui.w, kyi = li.w * Ui.y + li.y * Ui.w,
+                 kzi = li.w * Ui.z + li.z * Ui.w;
+    double zeta = 0.0, gx = 0.0, gy = 0.0, gz = 0.0, jx = 0.0, jy = 0.0, jz = 0.0, dv = 0.0,
+           dj = 0.0;
+    constexpr int CH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
+#pragma unroll
+    for (int k0 = 0; k0 < KCMAX; k0 += CH) {
+      CoefChunk<CH> cf;
+      coef_load<CH>(S, i, k0, cf);
+      asm volatile("" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int l = row[k0 + k];
+        const double vx = cf.v[k][0], vy = cf.v[k][1], vz = cf.v[k][2];
+        const double gcx = cf.v[k][3], gcy = cf.v[k][4], gcz = cf.v[k][5];
+        const double dx = cf.v[k][6], dy = cf.v[k][7], dz = cf.v[k][8];
+        const double4 Uj = sld(ts.x, l);
+        const double4 lj = sld(ts.U, l);
+        zeta += vx * (Uj.x - Ui.x) + vy * (Uj.y - Ui.y) + vz * (Uj.z - Ui.z);
+        const double Ej = 0.5 * (Uj.x * Uj.x + Uj.y * Uj.y + Uj.z * Uj.z) + S.g * Uj.w;
+        gx += gcx * (Ej - Ei);
+        gy += gcy * (Ej - Ei);
+        gz += gcz * (Ej - Ei);
+        const double ej = lj.x * Uj.x + lj.y * Uj.y + lj.z * Uj.z + S.g * Uj.w;
+        jx += gcx * (ej - ei);
+        jy += gcy * (ej - ei);
+        jz += gcz * (ej - ei);
+        dv += dx * (Uj.x * Uj.w + fxi) + dy * (Uj.y * Uj.w + fyi) + dz * (Uj.z * Uj.w + fzi);
+        dj += dx * ((lj.w * Uj.x + lj.x * Uj.w) + kxi) + dy * ((lj.w * Uj.y + lj.y * Uj.w) + kyi) +
+              dz * ((lj.w * Uj.z + lj.z * Uj.w) + kzi);
+      }
+    }
+    const double4 q = ldv(S.ne + i);  // (n, eta_n)
+    const double f = S.nf[i].w;
+    const double etaU = zeta + f;
+    const double px = q.y * Ui.z - q.z * Ui.y;  // n x U  (also P of F at U)
+    const double py = q.z * Ui.x - q.x * Ui.z;
+    const double pz = q.x * Ui.y - q.y * Ui.x;
+    const double nx = q.y * li.z - q.z * li.y;  // n x u_n (P of J)
+    const double ny = q.z * li.x - q.x * li.z;
+    const double nz = q.x * li.y - q.y * li.x;
+    double4 fs, js;
+    fs.x = -etaU * px - gx;
+    fs.y = -etaU * py - gy;
+    fs.z = -etaU * pz - gz;
+    fs.w = -dv;
+    js.x = -(nx * zeta) - q.w * px - jx;
+    js.y = -(ny * zeta) - q.w * py - jy;
+    js.z = -(nz * zeta) - q.w * pz - jz;
+    js.w = -dj;
+    return (fs - js) - S.gn[i];
   }
 };
 
@@ -709,9 +812,10 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     const short* rows = S.lnbr + (int64_t)e1off * 8;
     const double* lce1 = S.LcE1 + (int64_t)e1off * 6;
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
-    for (int base = 0; base < nE2; base += 2 * TPB) {
+    const int nEs = Step::kE1Only ? nE1 : nE2;  // cells staged in step 1
+    for (int base = 0; base < nEs; base += 2 * TPB) {
       const int ca = base + threadIdx.x, cb = ca + TPB;
-      const bool va = ca < nE2, vb = cb < nE2;
+      const bool va = ca < nEs, vb = cb < nEs;
       const int ga = va ? __ldg(map + ca) : 0;
       const int gb = vb ? __ldg(map + cb) : 0;
       double4 a0 = d4(0.0), a1 = d4(0.0), a2 = d4(0.0), b0 = d4(0.0), b1 = d4(0.0),
@@ -769,9 +873,11 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       }
       sst(ts.La, c, acc);
     };
-    for (int c = threadIdx.x; c < nE1; c += TPB)
-      lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
-    __syncthreads();
+    if (!Step::kE1Only) {
+      for (int c = threadIdx.x; c < nE1; c += TPB)
+        lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
+      __syncthreads();
+    }
     SRP_MARK(1)
     // step 3: z = scale * J x on the own cells
     if ((int)threadIdx.x < nT) {
@@ -779,9 +885,9 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       const int64_t i = c0 + c;
       const double4 ai = sld(ts.x, c);
       const double4 Ui = sld(ts.U, c);
-      const double4 lai = sld(ts.La, c);
+      const double4 lai = Step::kE1Only ? d4(0.0) : sld(ts.La, c);
       const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const Lrow lr = load_lrow(lce1 + (int64_t)c * 6);
+      const Lrow lr = Step::kE1Only ? Lrow{} : load_lrow(lce1 + (int64_t)c * 6);
       const double4 z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
