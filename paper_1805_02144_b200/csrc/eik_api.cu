@@ -151,17 +151,26 @@ __device__ int phase_rhs_step(cg::grid_group& grid, Smem& sm, const SweOp& S, co
 template <class Epi>
 __device__ int phase_dev(cg::grid_group& grid, Smem& sm, const SweOp& S,
                          const double4* U, const double4* fn, Epi epi,
-                         double* part) {
+                         double* part, const double4* Uadd = nullptr,
+                         double4* Ubuf = nullptr, bool keep_U = false) {
   if (S.tiled_ok) {
-    // one 1-ring tiled pass: [F*(U) - J*_n U] - g_n (DevStep)
+    // one 1-ring tiled pass: [F*(U) - J*_n U] - g_n (DevStep); with Uadd the
+    // stage state U + Uadd is formed on the fly, (U - (-1) Uadd) / 1 being
+    // exactly U + Uadd
     double r[1] = {0.0};
-    Form FD{U, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+    // (keep_U: U + Uadd is also stored to Ubuf, every cell being own in one tile)
+    Form FD{U, Uadd, nullptr, -1.0, 0.0, 1.0, (Uadd && keep_U) ? Ubuf : nullptr, nullptr};
     swe_tiled_op(sm, S, FD, DevStep{}, [&](int64_t i, double4 d, double4 w, double4) {
       epi(i, d);
       r[0] += nf4(d) + nf4(w);
     });
     grid_reduce<1>(grid, sm, r, part);
     return r[0] > 0.0 ? EIK_ENONFINITE : EIK_OK;
+  }
+  if (Uadd) {
+    pointwise(S.N, [&](int64_t i) { Ubuf[i] = U[i] + Uadd[i]; });
+    grid.sync();
+    U = Ubuf;
   }
   int64_t lo, hi;
   brange(S.N, lo, hi);
@@ -301,32 +310,25 @@ __device__ int step_call_setup(cg::grid_group& grid, Smem& sm, const SweArgs& A,
     st = phase_dev(grid, sm, A.S1, A.uprev, A.fn,
                    [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
   } else if (key == EIK_EXPRB42 * 4 + 1) {
-    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
-    grid.sync();
     const double c = (32.0 / 9.0) * dt;
-    st = phase_dev(grid, sm, A.S1, Ub, A.fn,
-                   [&](int64_t i, double4 d) { va[i] = c * d; }, A.Wk.part);
+    st = phase_dev(grid, sm, A.S1, u, A.fn, [&](int64_t i, double4 d) { va[i] = c * d; },
+                   A.Wk.part, W[0], Ub);
   } else if (key == EIK_PEXPRB43 * 4 + 1) {
-    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
-    grid.sync();
-    st = phase_dev(grid, sm, A.S1, Ub, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
-                   A.Wk.part);
+    st = phase_dev(grid, sm, A.S1, u, A.fn, [&](int64_t i, double4 d) { d2[i] = d; },
+                   A.Wk.part, W[0], Ub);
     if (st == EIK_OK) {
-      pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[1][i]; });  // U3
-      grid.sync();
-      st = phase_dev(grid, sm, A.S1, Ub, A.fn,
+      st = phase_dev(grid, sm, A.S1, u, A.fn,  // U3 = u + W1
                      [&](int64_t i, double4 d3) {
                        const double4 a = d2[i];
                        va[i] = dt * ((16.0 * a) - (2.0 * d3));
                        vb[i] = dt * ((-48.0 * a) + (12.0 * d3));
                      },
-                     A.Wk.part);
+                     A.Wk.part, W[1], Ub, true);  // Ub = U3: the base of u_{n+1}
     }
   } else if (key == EIK_EXPRB53 * 4 + 1) {
-    pointwise(A.S1.N, [&](int64_t i) { Ub[i] = u[i] + W[0][i]; });
-    grid.sync();
-    st = phase_dev(grid, sm, A.S1, Ub, A.fn,
-                   [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, A.Wk.part);
+    st = phase_dev(grid, sm, A.S1, u, A.fn,
+                   [&](int64_t i, double4 d) { d2[i] = d; va[i] = dt * d; }, A.Wk.part, W[0],
+                   Ub);
   } else if (key == EIK_EXPRB53 * 4 + 2) {
     const double c1 = 27.0 / 25.0, c2 = 729.0 / 125.0, q3 = A.c09cube;
     pointwise(A.S1.N, [&](int64_t i) {
