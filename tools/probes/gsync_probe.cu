@@ -1,7 +1,8 @@
 // Probe: cost of a grid barrier and of 5-value deterministic grid reductions on
-// 296 x 256-thread cooperative CTAs (mode 0: CTA-major partials, the round-1
-// baseline; 1: grid.sync alone; 2: last-arriver reduction; 3/7: value-major
-// variants -- 7 is what eik_dev.cuh's grid_reduce now does).
+// 296 x 256-thread cooperative CTAs (mode 0: eik_dev.cuh's grid_reduce, now
+// value-major; 1: grid.sync alone; 2: last-arriver reduction; 3/7: value-major
+// variants; 6: barrier + one partial load).  Measured: CTA-major partials
+// (round-1 baseline) 4.4 us, value-major 2.5 us, grid.sync 1.25 us.
 // nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -o gsync_probe gsync_probe.cu
 #include "../../paper_1805_02144_b200/csrc/eik_dev.cuh"
 #include <cstdio>
@@ -146,8 +147,6 @@ __global__ void __launch_bounds__(TPB, 2) k(double* part, double* out, long long
     else if (mode == 1) grid.sync();
     else if (mode == 2) grid_allreduce<5>(sm, d, part, bar, tot);
     else if (mode == 3) grid_reduce2<5>(grid, sm, d, part);
-    else if (mode == 4) { part_store<5>(sm, d, part); grid.sync(); }
-    else if (mode == 5) { grid.sync(); part_total<5>(sm, part, d); }
     else if (mode == 7) grid_reduce3<5>(grid, sm, d, part);
     else if (mode == 6) { grid.sync(); if (threadIdx.x < 5) sm.tot[threadIdx.x] = __ldcg(part + threadIdx.x); __syncthreads(); d[0] = sm.tot[0]; }
     acc += d[0] + d[4];
