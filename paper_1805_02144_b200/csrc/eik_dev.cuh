@@ -1796,11 +1796,15 @@ __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
     eps = broke ? 0.0 : eik_mul(eik_mul(beta, fabs(hnext)), fabs(corner));
   }
 
+  // the acceptance test needs only eps (phipm.py:336-341): the candidate is
+  // formed for accepted attempts only (a rejected one never reads it)
+  const bool accept = eik_div(eik_mul(E.t_out, eps), eik_mul(tau, T.tol)) <= T.delta;
+
   // ---- candidate (phipm.py:198-212, krylov.py:136-145)
   const int ycur = E.ycur;
   double4* cand = Wk.ybuf[ycur == 0 ? 1 : 0];
-  bool cand_nz;
-  {
+  bool cand_nz = false;
+  if (accept) {
     const double4* y = E.y;
     const double4* vz = E.vz;
     const double4* vm1 = E.vm1;
