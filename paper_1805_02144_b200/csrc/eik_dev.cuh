@@ -1052,64 +1052,78 @@ __device__ double blk_norm1(DenseRed& rs, const double* M, int n, int ld) {
 // (kernels.py:142).
 template <int NT>
 __device__ void blk_solve(DenseRed& rs, double* P, double* Q, int n, int ld) {
-  const int lane = threadIdx.x & 31;
+  static_assert(NT >= 64 && NT % 32 == 0, "blk_solve: at least two warps");
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned used = 0u;  // warp 0, bit q: row lane + 32 q is a pivot row already
-  for (int k = 0; k < n; ++k) {
-    // pivot (warp 0): |P[r][k]| compared as IEEE bit patterns (monotonic for
-    // x >= 0), reduced with three 32-bit warp reductions (hi, lo, row)
-    if (threadIdx.x < 32) {
-      unsigned long long key = 0ull;
-      int bi = n;
-      for (int q = 0; lane + 32 * q < n; ++q) {
-        const int r = lane + 32 * q;
-        if ((used >> q) & 1u) continue;
-        const unsigned long long b =
-            (unsigned long long)__double_as_longlong(fabs(P[(int64_t)r * ld + k]));
-        if (bi == n || b > key) { key = b; bi = r; }
-      }
-      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-      const unsigned hmax = __reduce_max_sync(0xffffffffu, bi < n ? hi : 0u);
-      const unsigned lmax = __reduce_max_sync(0xffffffffu, (bi < n && hi == hmax) ? lo : 0u);
-      const bool cand = bi < n && hi == hmax && lo == lmax;
-      const int pw = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)bi : 0xffffffffu);
-      if ((pw & 31) == lane) used |= 1u << (pw >> 5);
-      if (lane == 0) {
-        const double pk = P[(int64_t)pw * ld + k];
-        rs.piv[k] = pw;
-        rs.dg[k] = pk;
-        rs.rinv[k] = 1.0 / pk;
-      }
+  // pivot of column k (warp 0): |P[r][k]| compared as IEEE bit patterns
+  // (monotonic for x >= 0), reduced with three 32-bit warp reductions
+  auto pivot = [&](int k) {
+    unsigned long long key = 0ull;
+    int bi = n;
+    for (int q = 0; lane + 32 * q < n; ++q) {
+      const int r = lane + 32 * q;
+      if ((used >> q) & 1u) continue;
+      const unsigned long long b =
+          (unsigned long long)__double_as_longlong(fabs(P[(int64_t)r * ld + k]));
+      if (bi == n || b > key) { key = b; bi = r; }
     }
-    __syncthreads();
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned hmax = __reduce_max_sync(0xffffffffu, bi < n ? hi : 0u);
+    const unsigned lmax = __reduce_max_sync(0xffffffffu, (bi < n && hi == hmax) ? lo : 0u);
+    const bool cand = bi < n && hi == hmax && lo == lmax;
+    const int pw = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)bi : 0xffffffffu);
+    if ((pw & 31) == lane) used |= 1u << (pw >> 5);
+    if (lane == 0) {
+      const double pk = P[(int64_t)pw * ld + k];
+      rs.piv[k] = pw;
+      rs.dg[k] = pk;
+      rs.rinv[k] = 1.0 / pk;
+    }
+  };
+  if (w == 0) pivot(0);
+  __syncthreads();
+  // step k (one barrier): warp 0 eliminates column k+1 first and finds the
+  // next pivot from it (lookahead) while warps 1.. eliminate the other
+  // columns (P k+2 .. n-1, then Q 0 .. n-1); lanes -> columns, warps -> rows.
+  // Column k and the pivot row are only read in step k.
+  for (int k = 0; k < n; ++k) {
     const int p = rs.piv[k];
-    // eliminate column k from every other row: thread -> (column lane of a
-    // 128-wide chunk, row group); P columns k+1 .. n-1 then Q columns
-    // 0 .. n-1.  The pivot row and column k are only read in this step.
-    constexpr int CW = 128, RG = NT / CW;
-    static_assert(NT % CW == 0, "blk_solve: NT multiple of 128");
     const double rinv = rs.rinv[k];
-    const int np = n - k - 1;
-    const int nc = np + n;
-    const int cl = threadIdx.x % CW, g = threadIdx.x / CW;
-    for (int cb = 0; cb < nc; cb += CW) {
-      const int c = cb + cl;
-      if (c < nc) {
-        double* col = c < np ? P + (k + 1 + c) : Q + (c - np);
-        const double pv = col[(int64_t)p * ld];
-        for (int r0 = g; r0 < n; r0 += 4 * RG) {
-          double lv[4], v[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = r0 + q * RG;
-            const bool ok = r < n && r != p;
-            lv[q] = ok ? P[(int64_t)r * ld + k] : 0.0;
-            v[q] = ok ? col[(int64_t)r * ld] : 0.0;
+    if (w == 0) {
+      if (k + 1 < n) {
+        const double pv = P[(int64_t)p * ld + k + 1];
+        for (int r = lane; r < n; r += 32)
+          if (r != p) {
+            double* x = P + (int64_t)r * ld;
+            x[k + 1] = x[k + 1] - (x[k] * rinv) * pv;
           }
+        __syncwarp();
+        pivot(k + 1);
+      }
+    } else {
+      const int np = n - k - 2;  // P columns k+2 .. n-1
+      const int nc = (np > 0 ? np : 0) + n;
+      for (int c0 = 0; c0 < nc; c0 += 4 * 32) {
+        double* col[4];
+        double pv[4];
+        bool ok[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = r0 + q * RG;
-            if (r < n && r != p) col[(int64_t)r * ld] = v[q] - (lv[q] * rinv) * pv;
-          }
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + lane + 32 * q;
+          ok[q] = c < nc;
+          col[q] = c < np ? P + (k + 2 + c) : Q + (c - (np > 0 ? np : 0));
+          pv[q] = ok[q] ? col[q][(int64_t)p * ld] : 0.0;
+        }
+        for (int r = w - 1; r < n; r += NW - 1) {
+          if (r == p) continue;
+          const double l = P[(int64_t)r * ld + k] * rinv;
+          double v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = ok[q] ? col[q][(int64_t)r * ld] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ok[q]) col[q][(int64_t)r * ld] = v[q] - l * pv[q];
         }
       }
     }
