@@ -1002,6 +1002,7 @@ __device__ void blk_matmul(const double* A, const double* B, double* C, int n, i
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int q = 0; q < 4; ++q) c[r][q] = 0.0;
+#pragma unroll 4
     for (int k = 0; k < n; ++k) {
       double av[4], bv[4];
 #pragma unroll
