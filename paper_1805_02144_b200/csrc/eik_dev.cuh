@@ -1581,7 +1581,9 @@ __device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const E
     if constexpr (Op::kTiled) {
       if (tiled_mv) {
         ++mv;
-        Form F{wprev, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr};
+        // directions alternate back from the sweep's first iteration (rev 0):
+        // every pass starts on the tiles the previous one streamed last
+        Form F{wprev, nullptr, nullptr, 0.0, 0.0, 1.0, nullptr, nullptr, (p - j + 1) & 1};
         swe_tiled(sm, op, F,
                   [&](int64_t i, double4 z, double4, double4) {
                     double4 a = z;
