@@ -1306,7 +1306,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   // CTA to the same count with empty tiles
   // (measured: LPT scatters the tiles processed concurrently and loses the L2
   // locality of the halo gathers -- 182 vs 143 us per Krylov iteration at L8 --
-  // so it is off; round-robin keeps every wave a contiguous Hilbert region)
+  // so it is off; round-robin keeps every wave a contiguous range of the device order)
   int NTb = NT;
   if (EIK_LPT) {
     std::vector<double> cost(NT);

@@ -248,7 +248,7 @@ struct SweOp {
   const double* df1;     // [K][N] Df(i, slot) (0 where Df has no entry)
   const int* dfx;        // [N] nonzero Df entries outside the slot set
   const int* cnt;        // [N] valid slots
-  // tiled single-pass Krylov iteration (cells tiled along the Hilbert order;
+  // tiled single-pass Krylov iteration (tiles = contiguous ranges of the device cell order;
   // each tile's 2-ring halo is staged in shared memory)
   int ntiles;
   const int* t_cell0;    // first own cell

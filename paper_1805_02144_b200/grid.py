@@ -10,8 +10,8 @@ on its output, and so that the GPU path reads exactly the same operators.
 Grid: recursive bisection of the icosahedron to level ``L`` (N_g = 10*4^L+2
 nodes), one Voronoi control volume per node, nodes ordered
 along a 3-D Hilbert curve so that a cell's 5-6 neighbours sit close to it in
-memory (the same order is the reference's ``[u_x;u_y;u_z;h]`` layout and the
-device layout).
+memory (the order of the reference-facing ``[u_x;u_y;u_z;h]`` layout; libeik
+renumbers cells on the device into compact tiles, see eik_tile_order).
 
 Finite-volume operators on cell i with neighbours j (Voronoi edge e_ij of arc
 length l_ij, outward unit normal n_ij and counter-clockwise unit tangent t_ij
