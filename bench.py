@@ -10,7 +10,13 @@ workload on its own GPU, with no data-path collective; ``value`` is the sum of
 steps over ranks divided by the max-over-ranks device time ("weak" scaling).
 
 A step is one EXPRB4 step of the resident state: F(u_n), eta, n_A, two
-phipm/IOM2 engine calls, the stage perturbation -- one CUDA graph per step
+phipm/IOM2 engine calls, the stage perturbation.  Both arms time the same
+steps: trajectory steps 1-2 of the config from its seeded initial state with
+cold engine seeds (the reference arm's bounded CPU sample); the GPU arm
+replays that episode K times, restoring the initial state and seeds from a
+device-side snapshot at the start of each episode.  ``full_run`` adds the
+device time of the config's whole stated run (C3: 144 steps, one day).
+Each step is one CUDA graph
 (libeik's split step: a continuation kernel and, under a device-driven while
 node, one cooperative Krylov-sweep kernel ``k_swe_sweep`` per IOM2 sweep plus
 its dense phi kernel).  Timing: CUDA events recorded by libeik around every
@@ -145,13 +151,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline_oracle(ops, u0, spec, nsteps):
+EPISODE = 2  # trajectory steps timed by both arms (the reference arm's bounded sample)
+
+
+def workload(cfg, ops, spec, scheme):
+    """One workload string for both arms (the driver compares them)."""
+    return (f"{cfg}: L{ops.level} icosahedral ({ops.n_g} cells) {scheme} dt={spec.dt}s "
+            f"tol={spec.tol}; trajectory steps 1-{EPISODE} from the seeded initial state "
+            f"(cold engine seeds), replayed")
+
+
+def cpu_baseline_oracle(ops, u0, spec, scheme, nsteps):
     """The oracle port (numpy/scipy restatement of the reference) on the host
-    cores: ``nsteps`` steps from the config's initial state."""
+    cores: trajectory steps 1..nsteps from the config's initial state."""
     from oracle import integrate_oracle, swe_problem
     t = time.perf_counter()
-    integrate_oracle(swe_problem(ops), spec.scheme if spec.scheme else "exprb42", u0,
-                     spec.dt, nsteps * spec.dt, tol=spec.tol)
+    integrate_oracle(swe_problem(ops), scheme, u0, spec.dt, nsteps * spec.dt, tol=spec.tol)
     return time.perf_counter() - t
 
 
@@ -164,23 +179,22 @@ def run_reference(args):
         os.environ[k] = str(threads)
     from paper_1805_02144_b200.states import make_config
     ops, u0, spec = make_config(args.config, level=args.level)
-    spec.scheme = args.scheme
-    nsteps = max(1, min(args.steps, 2))
-    secs = cpu_baseline_oracle(ops, u0, spec, nsteps)
+    nsteps = EPISODE
+    secs = cpu_baseline_oracle(ops, u0, spec, args.scheme, nsteps)
     value = nsteps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
         "n_gpus": ws, "steps": nsteps, "warmup": 0, "ms_per_step": 1e3 * secs / nsteps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: L{ops.level} ({ops.n_g} cells) "
-                   f"{args.scheme} dt={spec.dt} tol={spec.tol}", "cells": ops.n_g},
+        "dtype": "f64", "data": "synthetic (seeded BASELINE C3 jet state on our icosahedral grid)",
+        "config": {"workload": workload(args.config, ops, spec, args.scheme),
+                   "cells": ops.n_g},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{nsteps} {args.scheme} step(s) of {args.config} from "
-                                   "the seeded initial state (cold engine seeds); "
-                                   "scipy csr_matvec is single-threaded, BLAS uses all "
-                                   "cores"},
+                         "sample": f"trajectory steps 1-{nsteps} of {args.config} "
+                                   f"{args.scheme} from the seeded initial state (cold engine "
+                                   "seeds), timed once; scipy csr_matvec is "
+                                   "single-threaded, BLAS uses all cores"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -188,11 +202,29 @@ def run_reference(args):
     return 0
 
 
+def self_launch(args):
+    """--gpus N without torchrun: re-run this script under torch.distributed.run
+    with N processes on this node (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
     if args.impl == "reference":
         return run_reference(args)
-    ws, rank, local = dist_env()
     dist = None
     if ws > 1:
         import torch
@@ -200,6 +232,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     import torch
+    from paper_1805_02144_b200 import _native as nat
     from paper_1805_02144_b200 import swe as gswe
     from paper_1805_02144_b200.states import make_config
 
@@ -207,24 +240,21 @@ def main():
     scheme = args.scheme
     ctx = gswe.SweContext(ops, device=local)
     ctx.set_state(u0)
+    ctx.set_prev(None)
     ctx.reset_seeds()
-    first = True
+    ctx.snapshot()  # trajectory start: initial state, cold seeds
 
-    def step():
-        nonlocal first
-        sch = "rb_euler" if (scheme == "epi3" and first) else scheme
-        first = False
+    def step(i):
+        """Timed unit: trajectory step (i mod EPISODE) + 1; the episode
+        restarts from the device snapshot of the initial state."""
+        k = i % EPISODE
+        if k == 0:
+            ctx.snapshot(restore=True)
+        sch = "rb_euler" if (scheme == "epi3" and k == 0) else scheme
         return ctx.step(sch, spec.dt, spec.tol)
 
-    from paper_1805_02144_b200 import _native as nat
     for w in range(args.warmup):
-        if w == args.warmup - 1:
-            u_prev_snap = ctx.get_state()
-        step()
-    # snapshot of the trajectory at the start of the timed region (state,
-    # previous state, warm-start seeds): the e2e leg replays the same steps
-    u_snap = ctx.get_state()
-    seeds_snap = {slot: ctx.seeds(slot) for slot in nat.SLOT_IDS}
+        step(w)
     torch.cuda.synchronize(local)
     if dist:
         dist.barrier()
@@ -236,8 +266,8 @@ def main():
     mv = 0
     t0 = time.perf_counter()
     step_ms = []
-    for _ in range(args.steps):
-        calls = step()
+    for i in range(args.steps):
+        calls = step(i)
         step_ms.append(ctx.last_kernel_ms())
         dev_ms += step_ms[-1]
         mv += sum(int(c.matvecs) for c in calls)
@@ -248,52 +278,61 @@ def main():
     clocks = clk.stop()
     launches = ctx.launches() - l0
     kiters = ctx.krylov_iters() - k0
-    from paper_1805_02144_b200.replicas import aggregate_throughput, max_over_ranks
+    from paper_1805_02144_b200.replicas import aggregate_throughput
     value, ms = aggregate_throughput(args.steps, dev_ms, dist, f"cuda:{local}")
     ms_per_step = ms / args.steps
 
-    # end to end through the C ABI: pinned host state in, step, state out
-    # -- the same first e2e_steps steps of the timed region, replayed from the
-    # snapshot; two pinned buffers used in turn (step k's result is step
-    # k+1's input)
-    def restore():
-        ctx.set_state(u_snap)
-        if scheme == "epi3":
-            ctx.set_prev(u_prev_snap)
-        for slot, (tau, m) in seeds_snap.items():
-            ctx.set_seeds(slot, tau, m)
-
-    pins = [torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory() for _ in range(2)]
+    # end to end through the C ABI: the same steps, each step's input state
+    # copied in from pinned host memory and its result copied back (step k's
+    # result is step k+1's input; an episode starts from the host initial
+    # state with cold seeds)
+    pins = [torch.empty(4 * ops.n_g, dtype=torch.float64).pin_memory() for _ in range(3)]
     bufs = [p.numpy() for p in pins]
-    bufs[0][:] = u_snap
-    restore()
+    bufs[2][:] = u0
     args.e2e_steps = args.steps if args.e2e_steps <= 0 else min(args.e2e_steps, args.steps)
     torch.cuda.synchronize(local)
     e2e_dev_ms = 0.0
     te = time.perf_counter()
-    for k in range(args.e2e_steps):
-        hin, hout = bufs[k & 1], bufs[(k + 1) & 1]
-        ctx.set_state(hin)
-        step()
+    for i in range(args.e2e_steps):
+        k = i % EPISODE
+        hin = bufs[2] if k == 0 else bufs[(i - 1) & 1]
+        hout = bufs[i & 1]
+        if k == 0:
+            ctx.set_prev(None)
+            ctx.reset_seeds()
+        nat.check(nat.load().eik_swe_set_state(ctx.h, nat.dptr(hin)), "set_state")
+        sch = "rb_euler" if (scheme == "epi3" and k == 0) else scheme
+        ctx.step(sch, spec.dt, spec.tol)
         e2e_dev_ms += ctx.last_kernel_ms()
         nat.check(nat.load().eik_swe_get_state(ctx.h, nat.dptr(hout)), "get_state")
     e2e_wall = time.perf_counter() - te
     e2e, _ = aggregate_throughput(args.e2e_steps, 1e3 * e2e_wall, dist, f"cuda:{local}")
 
-    # the dominant kernel alone: the timed steps replayed from the snapshot,
-    # launched kernel by kernel (host-loop mode, identical results), every
-    # Krylov sweep kernel bracketed by CUDA events on the libeik stream
+    # the dominant kernel alone: the timed steps replayed kernel by kernel
+    # (host-loop mode, identical results), every Krylov sweep kernel
+    # bracketed by CUDA events on the libeik stream
     nsw_steps = args.steps if args.sweep_steps <= 0 else min(args.sweep_steps, args.steps)
-    restore()
     ctx.set_hostloop(True)
     ctx.sweep_timing(reset=True)
     k1 = ctx.krylov_iters()
-    for _ in range(nsw_steps):
-        step()
+    for i in range(nsw_steps):
+        step(i)
     torch.cuda.synchronize(local)
     sweep_ms, nsweeps = ctx.sweep_timing(reset=True)
     sweep_iters = ctx.krylov_iters() - k1
     ctx.set_hostloop(False)
+
+    # the config's whole stated run (C3: 144 steps = 1 day) from the initial
+    # state, graph-replayed: the representative average over the trajectory
+    ctx.snapshot(restore=True)
+    day_ms, day_mv = 0.0, 0
+    kd = ctx.krylov_iters()
+    for k in range(spec.steps):
+        sch = "rb_euler" if (scheme == "epi3" and k == 0) else scheme
+        calls = ctx.step(sch, spec.dt, spec.tol)
+        day_ms += ctx.last_kernel_ms()
+        day_mv += sum(int(c.matvecs) for c in calls)
+    day_iters = ctx.krylov_iters() - kd
 
     hbm, src = peaks()
     balg = b_alg_per_iter(ops)
@@ -321,12 +360,17 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded BASELINE C3 jet state on our icosahedral grid)",
-        "config": {"workload": f"{args.config}: L{ops.level} icosahedral ({ops.n_g} cells) "
-                   f"{scheme} dt={spec.dt}s tol={spec.tol}",
+        "config": {"workload": workload(args.config, ops, spec, scheme),
                    "cells": ops.n_g, "parallelism": f"replicas x{ws}",
                    "l2": "no flush: inputs > L2 (each Krylov iteration streams ~0.5 GB)"},
         "krylov_iters_per_step": it_per_step, "matvecs_per_step": mv / args.steps,
         "wall_ms_per_step": 1e3 * wall / args.steps,
+        "full_run": {"steps": spec.steps, "device_ms": day_ms,
+                     "steps_per_s": 1e3 * spec.steps / day_ms,
+                     "matvecs_per_step": day_mv / spec.steps,
+                     "krylov_iters_per_step": day_iters / spec.steps,
+                     "note": f"the config's whole stated run ({spec.steps} x {spec.dt}s) from "
+                             "the initial state, device time of the step graphs"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
                      "kernel": "k_swe_sweep",
@@ -352,12 +396,11 @@ def main():
     }
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        spec.scheme = scheme
-        secs = cpu_baseline_oracle(ops, u0, spec, 1)
+        secs = cpu_baseline_oracle(ops, u0, spec, scheme, 1)
         line["cpu_baseline"] = {
             "value": 1.0 / secs, "unit": "steps/s", "cores": threads, "kind": "port",
-            "sample": f"1 {scheme} step of {args.config} from the initial state (oracle "
-                      "port, cold seeds); scipy csr_matvec single-threaded"}
+            "sample": f"trajectory step 1 of {args.config} {scheme} from the initial state "
+                      "(oracle port, cold seeds); scipy csr_matvec single-threaded"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -37,7 +37,8 @@ typedef enum {
   EIK_ENONFINITE = 2,  /* -> ValueError ("non-finite right-hand side")      */
   EIK_EPHIPM = 3,      /* -> PhipmFailure (substep budget exhausted)        */
   EIK_ECUDA = 4,       /* -> RuntimeError                                   */
-  EIK_ENOMEM = 5       /* -> MemoryError                                    */
+  EIK_ENOMEM = 5,      /* -> MemoryError                                    */
+  EIK_ECALLBACK = 6    /* host matvec callback failed: its exception re-raised */
 } eik_status;
 
 /* schemes (integrators.py:20 SCHEME_NAMES order) */
@@ -117,8 +118,12 @@ eik_status eik_tile_order(int64_t n, const double* px, const double* py, const d
 
 /* ---------------------------------------------------------------- SWE */
 /* ops[11] = Gx Gy Gz Dx Dy Dz Vx Vy Vz L Df (each n_g x n_g CSR).  The
- * device path applies Df as -nu * L(L .); the creation checks that the
- * given Df has the pattern of L@L. */
+ * device path applies Df as -nu * L(L .); creation returns EIK_EINVAL unless
+ * the given Df equals -nu * (L @ L) entry by entry (within 1e-12 of
+ * nu * sum_k |L_ik L_kj|; entries outside the pattern of L@L must be zero).
+ * m_max: Krylov basis capacity (at least min(100, 4 n_g), the step path's
+ * PhiTask default; eik_swe_phipm grows it for a larger task m_max, up to the
+ * dense cap of 256). */
 eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops,
                           const double* n_x, const double* n_y,
                           const double* n_z, const double* f,
@@ -158,8 +163,9 @@ eik_status eik_swe_phipm(EikSwe* ctx, const double* u_lin, double dt,
  * per-engine-call counters, *ncalls how many engine calls ran. */
 eik_status eik_swe_step(EikSwe* ctx, int32_t scheme, double dt, double tol,
                         EikPhipmInfo* calls, int32_t* ncalls);
-/* nsteps steps back to back without host synchronisation between them
- * (CUDA-graph replay); per-step counters summed into matvecs/substeps. */
+/* nsteps calls of eik_swe_step (each a CUDA-graph replay followed by one
+ * host synchronisation that reads the step's status and counters back);
+ * the counters are summed into matvecs/substeps; stops at the first error. */
 eik_status eik_swe_advance(EikSwe* ctx, int32_t scheme, double dt, double tol,
                            int32_t nsteps, int64_t* matvecs, int64_t* substeps);
 
@@ -167,6 +173,11 @@ eik_status eik_swe_advance(EikSwe* ctx, int32_t scheme, double dt, double tol,
 eik_status eik_swe_seeds(EikSwe* ctx, int32_t slot, double* tau, int64_t* m,
                          int32_t set);
 eik_status eik_swe_reset_seeds(EikSwe* ctx);
+/* device-side snapshot of the trajectory position (state, epi3 history,
+ * seeds): restore = 0 takes it, restore != 0 puts it back (stream-ordered
+ * device copies, no host synchronisation).  No reference counterpart: lets a
+ * caller replay the same steps (bench.py) without host traffic. */
+eik_status eik_swe_snapshot(EikSwe* ctx, int32_t restore);
 
 /* Krylov microbenchmark: reps IOM2 sweeps of dimension m (A = dt J(u)) on
  * direction v, device time of the whole launch in out[0] (ms), kept
@@ -211,6 +222,24 @@ eik_status eik_csr_phipm(EikCsr* ctx, double scale, int64_t nnz_override,
                          const EikPhiTask* task, double* W,
                          EikPhipmInfo* info, EikTraceRec* trace,
                          int64_t trace_cap, int64_t* trace_len);
+
+/* ------------------------------------------------ host matvec callback */
+/* The reference's MatvecOperator around an arbitrary callable
+ * (phipm.py:45-54, as_operator 73-84): the engine runs on the device and
+ * every matvec is one host round trip.  The callback gets x (n doubles) and
+ * writes y = A x (n doubles, both host memory owned by the context), returns
+ * 0 on success; any other value aborts the call with EIK_ECALLBACK.  It is
+ * invoked on the thread that called eik_cb_phipm, once per performed matvec
+ * (zero-skipped products are not requested), in the engine's order. */
+typedef int (*eik_matvec_fn)(void* user, const double* x, double* y, int64_t n);
+typedef struct EikCb EikCb;
+eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out);
+eik_status eik_cb_destroy(EikCb* ctx);
+/* A x = scale * callback(x); nnz is the operator's n_A for the cost model */
+eik_status eik_cb_phipm(EikCb* ctx, eik_matvec_fn matvec, void* user, double scale,
+                        int64_t nnz, const EikPhiTask* task, double* W,
+                        EikPhipmInfo* info, EikTraceRec* trace, int64_t trace_cap,
+                        int64_t* trace_len);
 
 #ifdef __cplusplus
 }

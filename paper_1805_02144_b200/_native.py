@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(_HERE, "libeik.so")
 
-EIK_OK, EIK_EINVAL, EIK_ENONFINITE, EIK_EPHIPM, EIK_ECUDA, EIK_ENOMEM = range(6)
+EIK_OK, EIK_EINVAL, EIK_ENONFINITE, EIK_EPHIPM, EIK_ECUDA, EIK_ENOMEM, EIK_ECALLBACK = range(7)
 SCHEME_IDS = {"rb_euler": 0, "epi3": 1, "exprb42": 2, "pexprb43": 3,
               "exprb53": 4}
 SLOT_IDS = {"rbe": 0, "epi3": 1, "exprb42/1": 2, "exprb42/2": 3,
@@ -52,6 +52,8 @@ class EikTraceRec(C.Structure):
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
+# int (*eik_matvec_fn)(void* user, const double* x, double* y, int64_t n)
+MATVEC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, _D, _D, C.c_int64)
 _SIGS = {
     "eik_last_error": (C.c_char_p, []),
     "eik_version": (C.c_int, []),
@@ -80,6 +82,7 @@ _SIGS = {
     "eik_swe_seeds": (C.c_int, [_P, C.c_int32, _D, C.POINTER(C.c_int64),
                                 C.c_int32]),
     "eik_swe_reset_seeds": (C.c_int, [_P]),
+    "eik_swe_snapshot": (C.c_int, [_P, C.c_int32]),
     "eik_swe_krylov_bench": (C.c_int, [_P, _D, _D, C.c_double, C.c_int32, C.c_int32, _D]),
     "eik_swe_info": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "eik_prof_read": (C.c_int, [_D, C.c_int]),
@@ -96,6 +99,11 @@ _SIGS = {
                                 C.POINTER(EikPhiTask), _D,
                                 C.POINTER(EikPhipmInfo), C.POINTER(EikTraceRec),
                                 C.c_int64, C.POINTER(C.c_int64)]),
+    "eik_cb_create": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "eik_cb_destroy": (C.c_int, [_P]),
+    "eik_cb_phipm": (C.c_int, [_P, MATVEC_FN, C.c_void_p, C.c_double, C.c_int64,
+                               C.POINTER(EikPhiTask), _D, C.POINTER(EikPhipmInfo),
+                               C.POINTER(EikTraceRec), C.c_int64, C.POINTER(C.c_int64)]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <cmath>
 #include <cstdio>
@@ -268,6 +269,9 @@ __device__ void pointwise(int64_t N, F f) {
   for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) f(i);
 }
 
+// PhiTask's default m_max (phipm.py:87-107), used by every step-path call
+constexpr int64_t kStepMMax = 100;
+
 __device__ EngineTask base_task(const SweArgs& A) {
   EngineTask T;
   for (int l = 0; l < MAXV; ++l) T.v[l] = nullptr;
@@ -277,7 +281,7 @@ __device__ EngineTask base_task(const SweArgs& A) {
   T.tau_init = -1.0;
   T.m_init = 1;
   T.iom = 2;
-  T.m_max = 100;
+  T.m_max = kStepMMax;
   T.max_attempts = 1000000;
   T.zero_skip = 1;
   return T;
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_swe_cont(SweArgs A) {
       }
       return;
     }
-    if (r == ER_FAIL) { cont_stop(A, EIK_EPHIPM); return; }
+    if (r == ER_FAIL) { cont_stop(A, eng_fail_status(sT, A.Wk)); return; }
     if (r == ER_DONE) {
       eng_epilogue(grid, sT, A.Wk, E);
       call = call + 1;
@@ -698,6 +702,21 @@ __global__ void __launch_bounds__(TPB, MINB) k_csr_phipm(CsrArgs A) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = st;
 }
 
+struct CbArgs {
+  HostOp H;
+  EngineWork Wk;
+  EngineTask task;
+  int* status;
+};
+
+__global__ void __launch_bounds__(TPB, MINB) k_cb_phipm(CbArgs A) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  cg::grid_group grid = cg::this_grid();
+  const int st = engine_call(grid, sm, A.H, A.task, A.Wk, A.Wk.nnz);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = st;
+}
+
 // ====================================================================== host
 
 namespace {
@@ -717,6 +736,18 @@ struct Bufs {
       e = cudaMemset(*p, 0, count * sizeof(T));
     }
     return e;
+  }
+  // free *p (allocated here) and allocate count elements in its place
+  template <class T>
+  cudaError_t regrow(T** p, size_t count) {
+    for (auto it = ptrs.begin(); it != ptrs.end(); ++it)
+      if (*it == (void*)*p) {
+        cudaFree(*it);
+        ptrs.erase(it);
+        break;
+      }
+    *p = nullptr;
+    return get(p, count);
   }
   void release() {
     for (void* p : ptrs) cudaFree(p);
@@ -833,7 +864,7 @@ struct EngineHost {
     CK(mem.get(&wk.zero, NU));
     CK(mem.get(&wk.part, (size_t)2 * NPART * part_stride(G)));
     CK(mem.get(&wk.H, (size_t)m_alloc * m_alloc));
-    CK(mem.get(&wk.scr, (size_t)6 * MAXDIM * MAXDIM));
+    CK(mem.get(&wk.scr, (size_t)6 * MAXDIM * dense_ld(MAXDIM)));
     CK(mem.get(&wk.phi, MAXDIM + 4));
     CK(mem.get(&wk.seeds, 2 * EIK_NUM_SLOTS));
     CK(mem.get(&info_d, 4));
@@ -850,6 +881,18 @@ struct EngineHost {
     wk.n = n;
     wk.m_alloc = m_alloc;
     return reset_seeds();
+  }
+  // grow the Krylov basis and H to m vectors (m <= min(n, MAXDIM))
+  eik_status reserve(int64_t m) {
+    m = std::min<int64_t>(std::min<int64_t>(m, n), MAXDIM);
+    if (m <= m_alloc) return EIK_OK;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamSynchronize(st));
+    CK(mem.regrow(&wk.basis, (size_t)m * NU));
+    CK(mem.regrow(&wk.H, (size_t)m * m));
+    m_alloc = m;
+    wk.m_alloc = m;
+    return EIK_OK;
   }
   eik_status reset_seeds() {
     std::vector<double> s(2 * EIK_NUM_SLOTS);
@@ -886,10 +929,12 @@ struct EngineHost {
       if (!(t->rho[i] > t->rho[i - 1])) return fail(EIK_EINVAL, "rho must be strictly ascending");
     if (!(t->tol > 0.0)) return fail(EIK_EINVAL, "tol must be positive");
     if (t->iom < 1) return fail(EIK_EINVAL, "iom must be >= 1");
-    const int64_t mcap = std::min<int64_t>(std::max(t->m_max, 1), n);
+    // m_cap = min(m_max, n) (phipm.py:302); the dense cap (kernels.py:20,
+    // 159-163) is checked when the basis would outgrow it, as the reference
+    // raises then, so the basis never needs more than MAXDIM vectors
+    const int64_t mcap = std::min<int64_t>(std::min<int64_t>(std::max(t->m_max, 1), n), MAXDIM);
     if (mcap > m_alloc)
       return fail(EIK_EINVAL, "m_max exceeds the context's basis allocation");
-    if (mcap + t->p + 1 > MAXDIM) return fail(EIK_EINVAL, "augmented dense size exceeds cap 256");
     return EIK_OK;
   }
   EngineTask make_task(const EikPhiTask* t) {
@@ -931,6 +976,8 @@ struct EngineHost {
       *trace_len = 0;
     }
     if (sth == EIK_EPHIPM) return fail(EIK_EPHIPM, "no convergence within the substep budget");
+    if (sth == EIK_EINVAL)
+      return fail(EIK_EINVAL, "augmented dense size exceeds cap 256");
     if (sth != EIK_OK) return fail((eik_status)sth, "engine failed");
     return EIK_OK;
   }
@@ -976,6 +1023,10 @@ struct EikSwe {
   unsigned long long kit_last = 0;
   float last_ms = 0.0f;
   double* pinned = nullptr;  // pinned staging for host copies (4N doubles)
+  // eik_swe_snapshot: device copy of (u, u_prev, seeds)
+  double4 *snap_u = nullptr, *snap_prev = nullptr;
+  double* snap_seeds = nullptr;
+  bool snap_have_prev = false;
 
   SweArgs args(double4* lin = nullptr, double dt = 1.0) {
     SweArgs A;
@@ -1046,6 +1097,15 @@ static const void* kSweKernels[] = {(const void*)k_swe_step, (const void*)k_swe_
                                     (const void*)k_swe_phipm, (const void*)k_swe_kbench,
                                     (const void*)k_swe_diag};
 static const void* kCsrKernels[] = {(const void*)k_csr_phipm};
+static const void* kCbKernels[] = {(const void*)k_cb_phipm};
+
+struct EikCb {
+  EngineHost eng;
+  HostOp H{};
+  double* xh = nullptr;  // mapped pinned host buffers
+  double* yh = nullptr;
+  unsigned int* mbox = nullptr;
+};
 
 extern "C" {
 
@@ -1127,6 +1187,48 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
         if (s >= 0) df1[(size_t)s * N + i] += Df.data[k];
         else if (Df.data[k] != 0.0) dfx[i] += 1;
       }
+  }
+  // ---- Df contract.  The device applies Df u as -nu * L(L u) (no 2-ring
+  // stencil streamed per Krylov iteration); the reference applies the given
+  // Df matrix (swe.py:163-167, 190).  Accept only operator sets whose Df is
+  // -nu * (L @ L): per entry |Df_ij + nu (LL)_ij| <= 1e-12 nu sum_k |L_ik L_kj|
+  // (rounding of the product, whatever its summation order), entries outside
+  // the pattern of L@L exactly zero.
+  {
+    const EikCsrView& L = ops[OP_L];
+    const EikCsrView& Df = ops[10];
+    std::vector<double> ll(N, 0.0), mag(N, 0.0), dv(N, 0.0);
+    std::vector<char> seen(N, 0);
+    std::vector<int32_t> touched;
+    const double anu = std::fabs(nu);
+    for (int64_t i = 0; i < N; ++i) {
+      touched.clear();
+      for (int32_t k = L.indptr[i]; k < L.indptr[i + 1]; ++k) {
+        const int32_t j = L.indices[k];
+        const double a = L.data[k];
+        for (int32_t k2 = L.indptr[j]; k2 < L.indptr[j + 1]; ++k2) {
+          const int32_t c2 = L.indices[k2];
+          const double v = a * L.data[k2];
+          ll[c2] += v;
+          mag[c2] += std::fabs(v);
+          if (!seen[c2]) { seen[c2] = 1; touched.push_back(c2); }
+        }
+      }
+      for (int32_t k = Df.indptr[i]; k < Df.indptr[i + 1]; ++k) {
+        const int32_t c2 = Df.indices[k];
+        dv[c2] += Df.data[k];
+        if (!seen[c2]) { seen[c2] = 1; touched.push_back(c2); }
+      }
+      bool ok = true;
+      for (int32_t c2 : touched) {
+        if (std::fabs(dv[c2] + nu * ll[c2]) > 1e-12 * anu * mag[c2]) ok = false;
+        ll[c2] = mag[c2] = dv[c2] = 0.0;
+        seen[c2] = 0;
+      }
+      if (!ok)
+        return fail(EIK_EINVAL, "Df must equal -nu * (L @ L): the device applies it as "
+                                "-nu * L(L u) (row " + std::to_string(i) + ")");
+    }
   }
   // ---- device cell order.  The Krylov pass works on tiles of <= TILE own
   // cells plus their 2-ring halo; the cells are renumbered so that every tile
@@ -1350,7 +1452,10 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   c->N = N;
   c->K = K;
   c->c09cube = std::pow(0.9, 3.0);
-  eik_status s = c->eng.init(device, N, 4 * N, std::min<int64_t>(std::max(m_max, 1), 4 * N),
+  // the step path's engine calls use PhiTask's default m_max = 100
+  // (phipm.py:87-107): the basis always holds min(100, n) vectors
+  eik_status s = c->eng.init(device, N, 4 * N,
+                             std::min<int64_t>(std::max<int64_t>(m_max, kStepMMax), 4 * N),
                              kSweKernels, 9, tile_smem_bytes(e1max, e2max), Gt);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   Bufs& B = c->eng.mem;
@@ -1585,6 +1690,17 @@ eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
                          EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
   if (!c || !u_lin || !W) return fail(EIK_EINVAL, "invalid arguments");
   EngineHost& E = c->eng;
+  if (task && task->m_max > E.m_alloc) {
+    // a larger m_max than the context was created for: grow the basis (the
+    // cached step graph holds the old pointers)
+    eik_status r = E.reserve(task->m_max);
+    if (r != EIK_OK) return r;
+    if (c->gexec) {
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+      c->g_scheme = -1;
+    }
+  }
   eik_status s = E.check_task(task);
   if (s != EIK_OK) return s;
   CK(cudaSetDevice(E.dev));
@@ -1832,6 +1948,31 @@ eik_status eik_swe_reset_seeds(EikSwe* c) {
   return c->eng.reset_seeds();
 }
 
+eik_status eik_swe_snapshot(EikSwe* c, int32_t restore) {
+  if (!c) return fail(EIK_EINVAL, "invalid arguments");
+  CK(cudaSetDevice(c->eng.dev));
+  const size_t vb = (size_t)c->N * sizeof(double4), sb = 2 * EIK_NUM_SLOTS * sizeof(double);
+  if (!c->snap_u) {
+    if (restore) return fail(EIK_EINVAL, "no snapshot taken");
+    CK(c->eng.mem.get(&c->snap_u, c->N));
+    CK(c->eng.mem.get(&c->snap_prev, c->N));
+    CK(c->eng.mem.get(&c->snap_seeds, 2 * EIK_NUM_SLOTS));
+  }
+  cudaStream_t st = c->eng.st;
+  if (restore) {
+    CK(cudaMemcpyAsync(c->u, c->snap_u, vb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->uprev, c->snap_prev, vb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->eng.wk.seeds, c->snap_seeds, sb, cudaMemcpyDeviceToDevice, st));
+    c->have_prev = c->snap_have_prev;
+  } else {
+    CK(cudaMemcpyAsync(c->snap_u, c->u, vb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->snap_prev, c->uprev, vb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->snap_seeds, c->eng.wk.seeds, sb, cudaMemcpyDeviceToDevice, st));
+    c->snap_have_prev = c->have_prev;
+  }
+  return EIK_OK;
+}
+
 
 eik_status eik_swe_krylov_bench(EikSwe* c, const double* u, const double* v, double dt,
                                 int32_t m, int32_t reps, double* out) {
@@ -1974,7 +2115,8 @@ eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max
   }
   EikCsr* c = new EikCsr();
   const int64_t NU = (n + 3) / 4;
-  eik_status s = c->eng.init(device, NU, n, std::min<int64_t>(std::max(m_max, 1), n),
+  eik_status s = c->eng.init(device, NU, n,
+                             std::min<int64_t>(std::min<int64_t>(std::max(m_max, 1), n), MAXDIM),
                              kCsrKernels, 1, kDenseSmemBytes);
   if (s != EIK_OK) { c->eng.release(); delete c; return s; }
   int *rp, *ci;
@@ -2014,6 +2156,10 @@ eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
                          EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
   if (!c || !W) return fail(EIK_EINVAL, "invalid arguments");
   EngineHost& E = c->eng;
+  if (task && task->m_max > E.m_alloc) {
+    eik_status r = E.reserve(task->m_max);
+    if (r != EIK_OK) return r;
+  }
   eik_status s = E.check_task(task);
   if (s != EIK_OK) return s;
   CK(cudaSetDevice(E.dev));
@@ -2040,6 +2186,116 @@ eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
   CK(cudaLaunchCooperativeKernel((const void*)k_csr_phipm, E.G, TPB, kargs, E.smem, E.st));
   ++E.launches;
   s = E.finish_phipm(info, trace, trace_cap, trace_len);
+  if (s != EIK_OK) return s;
+  for (int i = 0; i < task->ns; ++i)
+    CK(cudaMemcpyAsync(W + (size_t)i * n, E.wout[i], n * sizeof(double), cudaMemcpyDeviceToHost, E.st));
+  CK(cudaStreamSynchronize(E.st));
+  return EIK_OK;
+}
+
+// ------------------------------------------------- host-callback operator
+eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out) {
+  if (!out || n < 1) return fail(EIK_EINVAL, "invalid arguments");
+  EikCb* c = new EikCb();
+  const int64_t NU = (n + 3) / 4;
+  eik_status s = c->eng.init(device, NU, n,
+                             std::min<int64_t>(std::min<int64_t>(std::max(m_max, 1), n), MAXDIM),
+                             kCbKernels, 1, kDenseSmemBytes);
+  auto bail = [&](eik_status st, const char* msg) {
+    if (c->xh) cudaFreeHost(c->xh);
+    if (c->yh) cudaFreeHost(c->yh);
+    if (c->mbox) cudaFreeHost(c->mbox);
+    c->eng.release();
+    delete c;
+    return fail(st, msg);
+  };
+  if (s != EIK_OK) return bail(s, "engine init failed");
+  if (cudaHostAlloc((void**)&c->xh, n * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->yh, n * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->mbox, 64, cudaHostAllocMapped) != cudaSuccess)
+    return bail(EIK_ENOMEM, "mapped host allocation failed");
+  HostOp& H = c->H;
+  H.n = n;
+  H.NUu = NU;
+  if (cudaHostGetDevicePointer((void**)&H.xh, c->xh, 0) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&H.yh, c->yh, 0) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&H.mbox, c->mbox, 0) != cudaSuccess)
+    return bail(EIK_ECUDA, "mapped host pointers unavailable");
+  if (c->eng.mem.get(&H.ctr, 2) != cudaSuccess || c->eng.mem.get(&H.abort, 1) != cudaSuccess)
+    return bail(EIK_ENOMEM, "device allocation failed");
+  H.scale = 1.0;
+  *out = c;
+  return EIK_OK;
+}
+
+eik_status eik_cb_destroy(EikCb* c) {
+  if (!c) return EIK_OK;
+  cudaFreeHost(c->xh);
+  cudaFreeHost(c->yh);
+  cudaFreeHost(c->mbox);
+  c->eng.release();
+  delete c;
+  return EIK_OK;
+}
+
+eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale, int64_t nnz,
+                        const EikPhiTask* task, double* W, EikPhipmInfo* info,
+                        EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (!c || !W || !matvec) return fail(EIK_EINVAL, "invalid arguments");
+  EngineHost& E = c->eng;
+  if (task && task->m_max > E.m_alloc) {
+    eik_status r = E.reserve(task->m_max);
+    if (r != EIK_OK) return r;
+  }
+  eik_status s = E.check_task(task);
+  if (s != EIK_OK) return s;
+  CK(cudaSetDevice(E.dev));
+  if ((s = E.ensure_io()) != EIK_OK) return s;
+  const int64_t n = E.n;
+  for (int l = 0; l <= task->p; ++l) {
+    CK(cudaMemsetAsync(E.vin[l], 0, E.NU * sizeof(double4), E.st));
+    if (task->v && task->v[l])
+      CK(cudaMemcpyAsync(E.vin[l], task->v[l], n * sizeof(double), cudaMemcpyHostToDevice, E.st));
+  }
+  if (trace && trace_cap > 0 && (s = E.ensure_trace(trace_cap)) != EIK_OK) return s;
+  CbArgs A;
+  memset(&A, 0, sizeof(A));
+  A.H = c->H;
+  A.H.scale = scale;
+  A.Wk = E.wk;
+  A.Wk.nnz = nnz;
+  A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
+  A.Wk.trace_cap = (trace && trace_cap > 0) ? trace_cap : 0;
+  A.task = E.make_task(task);
+  A.status = E.status_d;
+  volatile unsigned int* mb = c->mbox;
+  mb[0] = 0;
+  mb[1] = 0;
+  CK(cudaMemsetAsync(c->H.ctr, 0, 2 * sizeof(unsigned long long), E.st));
+  CK(cudaMemsetAsync(c->H.abort, 0, sizeof(int), E.st));
+  CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
+  void* kargs[] = {&A};
+  CK(cudaLaunchCooperativeKernel((const void*)k_cb_phipm, E.G, TPB, kargs, E.smem, E.st));
+  ++E.launches;
+  // serve the kernel's matvec requests until it finishes
+  unsigned int served = 0;
+  bool cb_failed = false;
+  for (;;) {
+    const unsigned int req = mb[0];
+    if (req != served) {
+      const int rc = cb_failed ? 1 : matvec(user, c->xh, c->yh, n);
+      if (rc != 0) cb_failed = true;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      mb[1] = rc == 0 ? req : kCbAbort;
+      served = req;
+      continue;
+    }
+    const cudaError_t q = cudaStreamQuery(E.st);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(EIK_ECUDA, cudaGetErrorString(q));
+  }
+  s = E.finish_phipm(info, trace, trace_cap, trace_len);
+  if (cb_failed) return fail(EIK_ECALLBACK, "matvec callback failed");
   if (s != EIK_OK) return s;
   for (int i = 0; i < task->ns; ++i)
     CK(cudaMemcpyAsync(W + (size_t)i * n, E.wout[i], n * sizeof(double), cudaMemcpyDeviceToHost, E.st));

@@ -931,6 +931,35 @@ struct CsrOp {
   __device__ __forceinline__ int64_t NU() const { return NUu; }
 };
 
+// Host-callback operator (the reference's MatvecOperator around an arbitrary
+// callable, phipm.py:45-54): the engine stays on the device and every matvec
+// is a round trip through a mailbox in mapped pinned host memory.  All CTAs
+// write their part of x to xh and arrive on a device counter; the lead
+// thread posts a request sequence number and spins (nanosleep) until the
+// host thread serving eik_cb_phipm has written y = A x to yh and echoed the
+// number (or an abort code); the engine's grid barrier after op_pre then
+// releases every CTA to read yh.  Slow by construction (PCIe + the callable
+// per matvec), as SURVEY.md §8(b)(1) allows for this plug point.
+struct HostOp {
+  static constexpr bool kTiled = false;
+  int64_t n, NUu;
+  double* xh;                     // mapped host buffer (device address), n doubles
+  const double* yh;               // mapped host buffer, n doubles, written by the host
+  volatile unsigned int* mbox;    // mapped: [0] request seq, [1] reply seq / kCbAbort
+  unsigned long long* ctr;        // device: [0] CTA arrivals, [1] requests posted
+  int* abort;                     // device: 1 once the host aborted (or timed out)
+  double scale;
+  __device__ __forceinline__ int64_t NU() const { return NUu; }
+};
+constexpr unsigned int kCbAbort = 0xFFFFFFFFu;
+constexpr unsigned long long kCbTimeoutNs = 600ull * 1000000000ull;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ------------------------------------------------- operator "pre" + "main"
 // pre: everything a matvec needs before its main phase that reads other
 // CTAs' output (SWE: L x into lapA, scaled by inv).  main: (A x)(unit).
@@ -943,6 +972,70 @@ __device__ __forceinline__ void op_pre(const SweOp& S, const double4* x,
 }
 __device__ __forceinline__ void op_pre(const CsrOp&, const double4*, double,
                                        int64_t, int64_t) {}
+
+__device__ __forceinline__ void op_pre(const HostOp&, const double4*, double,
+                                       int64_t, int64_t) {}
+
+// op_pre with the exact vector the matvec is applied to (`formed`: v_j =
+// raw / h already written by this thread for u in [lo, hi)); only the host
+// operator needs it, the others recompute from raw and inv.
+template <class Op>
+__device__ __forceinline__ void op_pre_x(const Op& op, const double4* raw, double inv,
+                                         const double4* formed, int64_t lo, int64_t hi) {
+  op_pre(op, raw, inv, lo, hi);
+}
+template <>
+__device__ __forceinline__ void op_pre_x<HostOp>(const HostOp& H, const double4*, double,
+                                                 const double4* formed, int64_t lo,
+                                                 int64_t hi) {
+  if (*((volatile int*)H.abort)) return;
+  for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) {
+    const double4 a = formed[u];
+    const double c[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * u + q < H.n) H.xh[4 * u + q] = c[q];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(H.ctr, 1ull);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long k = H.ctr[1] + 1;
+    const unsigned long long target = k * gridDim.x;
+    while (atomicAdd(H.ctr, 0ull) < target) __nanosleep(64);
+    H.ctr[1] = k;
+    __threadfence_system();
+    const unsigned int seq = (unsigned int)(k & 0x7FFFFFFFu);
+    H.mbox[0] = seq;
+    __threadfence_system();
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned int r;
+    while ((r = H.mbox[1]) != seq && r != kCbAbort) {
+      __nanosleep(2000);
+      if (globaltimer_ns() - t0 > kCbTimeoutNs) { r = kCbAbort; break; }
+    }
+    if (r == kCbAbort) *((volatile int*)H.abort) = 1;
+    __threadfence_system();
+  }
+}
+
+__device__ __forceinline__ double4 op_main(const HostOp& H, const double4*, int64_t u) {
+  double r[4] = {0.0, 0.0, 0.0, 0.0};
+  if (!*((volatile int*)H.abort)) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * u + q < H.n) r[q] = H.scale * __ldcv(H.yh + 4 * u + q);
+  }
+  return make_double4(r[0], r[1], r[2], r[3]);
+}
+
+// true once a host-operator call was aborted (uniform after a grid barrier)
+template <class Op>
+__device__ __forceinline__ bool op_aborted(const Op&) { return false; }
+template <>
+__device__ __forceinline__ bool op_aborted<HostOp>(const HostOp& H) {
+  return *((volatile int*)H.abort) != 0;
+}
 
 __device__ __forceinline__ double4 op_main(const SweOp& S, const double4* x,
                                            int64_t i) {
@@ -1515,6 +1608,29 @@ __device__ bool eng_prologue(cg::grid_group& grid, Smem& sm, const EngineTask& T
   return true;
 }
 
+// A failed call: counters and status (EIK_EPHIPM: attempt budget exhausted,
+// phipm.py:321-330; EIK_EINVAL: dense size cap) into the call's info record.
+__device__ void eng_fail(cg::grid_group& grid, const EngineTask& T, const EngineWork& Wk, ES& E,
+                         int status) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    EikPhipmInfo inf = {};
+    inf.substeps = E.acc;
+    inf.rejections = E.rej;
+    inf.matvecs = E.mv;
+    inf.tau_final = E.tau;
+    inf.m_final = E.m;
+    inf.t_reached = E.t;
+    inf.attempts = E.attempts;
+    inf.status = status;
+    Wk.info[T.info_idx] = inf;
+  }
+  __threadfence();
+  grid.sync();
+}
+__device__ __forceinline__ int eng_fail_status(const EngineTask& T, const EngineWork& Wk) {
+  return __ldcg(&Wk.info[T.info_idx].status);
+}
+
 // Next attempt: write finished output points, then the w recurrence
 // (phipm.py:159-182) and the Krylov set-up.  ER_DONE: every output written;
 // ER_FAIL: attempt budget exhausted (info written); ER_SWEEP: the tiled IOM2
@@ -1537,21 +1653,14 @@ __device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const E
     E.io = E.io + 1;
     if (E.io < T.ns) E.t_out = T.rho[E.io];
   }
+  if (op_aborted(op)) {
+    eng_fail(grid, T, Wk, E, EIK_ECALLBACK);
+    return ER_FAIL;
+  }
   E.attempts = E.attempts + 1;
   if (E.attempts > T.max_attempts) {
-    if (lead) {
-      EikPhipmInfo inf = {};
-      inf.substeps = E.acc;
-      inf.rejections = E.rej;
-      inf.matvecs = E.mv;
-      inf.tau_final = E.tau;
-      inf.m_final = E.m;
-      inf.t_reached = E.t;
-      inf.attempts = E.attempts - 1;
-      inf.status = EIK_EPHIPM;
-      Wk.info[T.info_idx] = inf;
-    }
-    grid.sync();
+    E.attempts = E.attempts - 1;
+    eng_fail(grid, T, Wk, E, EIK_EPHIPM);
     return ER_FAIL;
   }
   E.tau_nom = E.tau;
@@ -1597,7 +1706,7 @@ __device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const E
     }
     if (!tiled_mv) {
       if (do_mv) {
-        op_pre(op, wprev, 1.0, lo, hi);
+        op_pre_x(op, wprev, 1.0, wprev, lo, hi);
         grid.sync();
         ++mv;
       }
@@ -1649,6 +1758,13 @@ __device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const E
   E.beta = beta;
   const int64_t m_eff = E.m < n ? E.m : n;
   const int64_t iom = m_eff < n ? T.iom : n;
+  if (m_eff + p + 1 > MAXDIM || m_eff > Wk.m_alloc) {
+    // kernels.py:159-163 raises ValueError once the augmented matrix would
+    // exceed DENSE_SIZE_CAP (256); the basis holds at most 255 - p vectors
+    E.mv = E.mv + mv;
+    eng_fail(grid, T, Wk, E, EIK_EINVAL);
+    return ER_FAIL;
+  }
   E.m_eff = m_eff;
   E.keep = m_eff;
   if (blockIdx.x == 0) {
@@ -1669,7 +1785,7 @@ __device__ int eng_attempt(cg::grid_group& grid, Smem& sm, const Op& op, const E
     const double4* vjm = j > 0 ? Wk.basis + (j - 1) * NU : nullptr;
     // v_j = raw / h (exact division), La = L v_j
     for (int64_t u = lo + threadIdx.x; u < hi; u += TPB) vj[u] = div4(raw[u], hcur);
-    op_pre(op, raw, 1.0 / hcur, lo, hi);
+    op_pre_x(op, raw, 1.0 / hcur, vj, lo, hi);
     grid.sync();
     // z = A v_j + projections
     double d[3] = {0.0, 0.0, 0.0};
@@ -1866,16 +1982,21 @@ __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
   const int64_t m = E.m, attempts = E.attempts;
   const double omega = eik_div(eik_mul(t_out, eps), eik_mul(tau, T.tol));
   const bool ok = omega <= T.delta;
-  if (lead && Wk.trace && attempts <= Wk.trace_cap) {
-    EikTraceRec tr;
-    tr.attempt = attempts;
-    tr.t = t;
-    tr.tau = tau;
-    tr.m = m;
-    tr.eps_m = eps;
-    tr.omega = omega;
-    tr.accepted = ok ? 1 : 0;
-    Wk.trace[attempts - 1] = tr;
+  if (lead && Wk.trace) {
+    // the trace is unbounded (phipm.py:341-343): trace_len counts every
+    // attempt, rows beyond the buffer are dropped and the host re-runs the
+    // (deterministic) call with a buffer of trace_len rows
+    if (attempts <= Wk.trace_cap) {
+      EikTraceRec tr;
+      tr.attempt = attempts;
+      tr.t = t;
+      tr.tau = tau;
+      tr.m = m;
+      tr.eps_m = eps;
+      tr.omega = omega;
+      tr.accepted = ok ? 1 : 0;
+      Wk.trace[attempts - 1] = tr;
+    }
     *Wk.trace_len = attempts;
   }
   Adapt ad = adapt_parameters(tau, m, t, eps, nh, t_out, T.rho[T.ns - 1], p, T.tol, T.delta,
@@ -1934,7 +2055,7 @@ __device__ int engine_call(cg::grid_group& grid, Smem& sm, const Op& op,
       eng_epilogue(grid, T, Wk, E);
       return EIK_OK;
     }
-    if (r == ER_FAIL) return EIK_EPHIPM;
+    if (r == ER_FAIL) return eng_fail_status(T, Wk);
     if constexpr (Op::kTiled) {
       if (r == ER_SWEEP) {
         ProfClock pc;

@@ -22,7 +22,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import swe as _swe
-from .phipm import CsrDeviceOperator, PhiTask, phipm_simul_iom2
+from .phipm import (CsrDeviceOperator, HostMatvecOperator, MatvecOperator, PhiTask,
+                    phipm_simul_iom2)
 from .sparse import SparseMatrix
 
 SCHEME_NAMES = ("rb_euler", "epi3", "exprb42", "pexprb43", "exprb53")
@@ -112,9 +113,11 @@ def _swe_step(problem, scheme, u_n, dt, tol, seeds, stats, u_prev=None):
             raise ValueError("epi3 requires the previous state")
         ctx.set_prev(u_prev)
     slots = _SLOTS[scheme]
-    if seeds is not None:
-        for s in slots:
-            ctx.set_seeds(s, *seeds.get(s))
+    # seeds=None starts every engine call cold, (tau, m) = (None, 1)
+    # (integrators.py:128); the context's device seeds from an earlier call
+    # must not leak into this one.
+    for s in slots:
+        ctx.set_seeds(s, *(seeds.get(s) if seeds is not None else (None, 1)))
     calls = ctx.step(scheme, dt, tol)
     if seeds is not None:
         for s, c in zip(slots, calls):
@@ -133,6 +136,8 @@ def _device_jacobian(problem, u):
     J = problem.jacobian(u)
     if isinstance(J, _swe.SweJacobian):
         return J
+    if isinstance(J, MatvecOperator):
+        return HostMatvecOperator(J)
     if not isinstance(J, SparseMatrix):
         J = SparseMatrix(J)
     return CsrDeviceOperator(J.csr)
@@ -177,6 +182,8 @@ def _engine(A, vectors, rho, tol, seeds, slot, stats):
 def _matvec(J, x):
     if isinstance(J, CsrDeviceOperator):
         return J.csr @ x  # host-side stage algebra on the user's own matrix
+    if isinstance(J, HostMatvecOperator):
+        return J.op.matvec(x)  # the user's own host callable
     return J.matvec(x)
 
 

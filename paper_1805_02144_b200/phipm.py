@@ -11,9 +11,10 @@ this module only validates the task and moves vectors across the C ABI.
 Operators the device engine accepts: ``SparseMatrix`` / scipy sparse /
 dense ``ndarray`` (a device CSR operator), a ``DeviceOperator`` such as
 ``swe.assemble_jacobian(ops, u)`` or ``scaled(op, dt)``, or a
-``MatvecOperator`` built over one of those.  A ``MatvecOperator`` around an
-arbitrary Python callable cannot run inside the device engine and raises
-``TypeError`` (the product path has no host fallback).
+``MatvecOperator``.  A ``MatvecOperator`` around an arbitrary Python callable
+keeps the engine on the device and calls back to the host for every matvec
+(``eik_cb_phipm``: a mailbox in mapped memory, one PCIe round trip per
+product); everything else about the call is identical.
 """
 
 import csv
@@ -27,6 +28,7 @@ from . import _native as nat
 from .sparse import SparseMatrix
 
 MAX_SUBSTEPS = 10 ** 6
+DENSE_SIZE_CAP = 256        # kernels.py:20
 CRAWL_SUBSTEPS = 100
 PADE13_THETA = 5.37
 
@@ -98,6 +100,24 @@ def as_operator(A, n=None):
     raise TypeError(f"cannot interpret {type(A)!r} as an operator")
 
 
+class HostMatvecOperator(DeviceOperator):
+    """A ``MatvecOperator`` around an arbitrary host callable: the engine runs
+    on the device and requests every matvec from the host through a mailbox
+    in mapped memory (``eik_cb_phipm``): one PCIe round trip plus the
+    callable per performed product -- slow, as the plug point allows."""
+
+    kind = "host"
+
+    def __init__(self, op, scale=1.0):
+        self.op = op
+        self.n = int(op.n)
+        self.nnz = int(op.nnz)
+        self.scale = float(scale)
+
+    def scaled(self, alpha):
+        return HostMatvecOperator(self.op, self.scale * float(alpha))
+
+
 def _device_operator(op):
     if isinstance(op, DeviceOperator):
         return op
@@ -105,10 +125,63 @@ def _device_operator(op):
         dev = getattr(op, "device", None) or getattr(op._matvec, "device", None)
         if isinstance(dev, DeviceOperator):
             return dev
-        raise TypeError(
-            "MatvecOperator around a host callable cannot run in the device "
-            "engine; pass a SparseMatrix/ndarray or a DeviceOperator")
+        return HostMatvecOperator(op)
     return as_operator(op)
+
+
+_CB_CACHE = {}
+
+
+def _cb_context(n, m_cap):
+    key = (n, m_cap)
+    ctx = _CB_CACHE.get(key)
+    if ctx is None:
+        h = nat.C.c_void_p()
+        nat.check(nat.load().eik_cb_create(n, 0, int(m_cap), nat.C.byref(h)), "eik_cb_create")
+        ctx = _CbCtx(h)
+        if len(_CB_CACHE) > 4:
+            _CB_CACHE.clear()
+        _CB_CACHE[key] = ctx
+    return ctx
+
+
+class _CbCtx:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            nat.load().eik_cb_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _run_host_callback(op, t, W, info, trace, cap, tlen):
+    """eik_cb_phipm with op.op.matvec as the callback; an exception raised by
+    the callable aborts the device engine and is re-raised here."""
+    n = op.n
+    failure = []
+
+    def cb(_user, xp, yp, nn):
+        try:
+            x = np.ctypeslib.as_array(xp, shape=(nn,)).copy()
+            y = np.asarray(op.op.matvec(x), dtype=float)
+            if y.shape != (nn,):
+                raise ValueError(f"matvec returned shape {y.shape}, expected ({nn},)")
+            np.ctypeslib.as_array(yp, shape=(nn,))[:] = y
+            return 0
+        except BaseException as e:  # noqa: BLE001 -- re-raised after the call
+            failure.append(e)
+            return 1
+
+    fn = nat.MATVEC_FN(cb)
+    ctx = _cb_context(n, min(max(t.m_max, 1), n, DENSE_SIZE_CAP))
+    st = nat.load().eik_cb_phipm(ctx.h, fn, None, op.scale, op.nnz, nat.C.byref(t),
+                                 nat.dptr(W), nat.C.byref(info), trace, cap,
+                                 nat.C.byref(tlen))
+    if failure:
+        raise failure[0]
+    return st
 
 
 @dataclass
@@ -218,20 +291,30 @@ def _run(task, op):
     t, keep = nat.make_task(task.v, task.rho, task.tol, task.m_init, task.iom,
                             task.m_max, task.delta, task.tau_init,
                             task.zero_skip, MAX_SUBSTEPS)
-    info = nat.EikPhipmInfo()
     cap = 4096 if task.trace else 0
-    trace = (nat.EikTraceRec * max(cap, 1))()
-    tlen = nat.C.c_int64(0)
-    W = np.zeros((ns, n))
-    if op.kind == "csr":
-        ctx = _csr_context(op, min(max(task.m_max, 1), n))
-        st = lib.eik_csr_phipm(ctx.h, op.scale, int(op.nnz), nat.C.byref(t),
-                               nat.dptr(W), nat.C.byref(info),
-                               trace if cap else None, cap, nat.C.byref(tlen))
-    elif op.kind == "swe":
-        st = op.run_phipm(t, W, info, trace if cap else None, cap, tlen)
-    else:
-        raise TypeError(f"unsupported device operator {op!r}")
+    while True:
+        info = nat.EikPhipmInfo()
+        trace = (nat.EikTraceRec * max(cap, 1))()
+        tlen = nat.C.c_int64(0)
+        W = np.zeros((ns, n))
+        if op.kind == "csr":
+            ctx = _csr_context(op, min(max(task.m_max, 1), n, DENSE_SIZE_CAP))
+            st = lib.eik_csr_phipm(ctx.h, op.scale, int(op.nnz), nat.C.byref(t),
+                                   nat.dptr(W), nat.C.byref(info),
+                                   trace if cap else None, cap, nat.C.byref(tlen))
+        elif op.kind == "swe":
+            st = op.run_phipm(t, W, info, trace if cap else None, cap, tlen)
+        elif op.kind == "host":
+            st = _run_host_callback(op, t, W, info, trace if cap else None, cap, tlen)
+        else:
+            raise TypeError(f"unsupported device operator {op!r}")
+        # the trace is unbounded (phipm.py:341-343): the device counts every
+        # attempt; a call with more attempts than the buffer holds is re-run
+        # (deterministically) with a buffer of the right size
+        if cap and st == nat.EIK_OK and tlen.value > cap:
+            cap = int(tlen.value)
+            continue
+        break
     if st == nat.EIK_EPHIPM:
         raise PhipmFailure(
             f"no convergence within {MAX_SUBSTEPS} substeps "

@@ -24,6 +24,11 @@ class SparseMatrix:
         self.csr = csr
 
     @classmethod
+    def identity(cls, n):
+        """kernels.py:49-51."""
+        return cls(scipy.sparse.identity(n, format="csr"))
+
+    @classmethod
     def from_dense(cls, a):
         return cls(np.asarray(a, dtype=float))
 
@@ -53,6 +58,17 @@ class SparseMatrix:
 
     def matvec(self, x):
         return self.csr @ x
+
+    def __matmul__(self, other):
+        """kernels.py:84-87: SparseMatrix @ SparseMatrix stays sparse."""
+        if isinstance(other, SparseMatrix):
+            return SparseMatrix(self.csr @ other.csr)
+        return self.csr @ other
+
+    def scaled(self, alpha):
+        """kernels.py:89-90: alpha * M, entries kept as scipy keeps them
+        (scalar scaling keeps explicit zeros, so nnz is unchanged)."""
+        return SparseMatrix(self.csr * float(alpha))
 
     def toarray(self):
         return self.csr.toarray()

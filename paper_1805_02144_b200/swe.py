@@ -135,6 +135,10 @@ class SweContext:
     def reset_seeds(self):
         nat.check(nat.load().eik_swe_reset_seeds(self.h), "reset_seeds")
 
+    def snapshot(self, restore=False):
+        """Device-side save (or restore) of state, epi3 history and seeds."""
+        nat.check(nat.load().eik_swe_snapshot(self.h, 1 if restore else 0), "snapshot")
+
     def launches(self):
         return int(nat.load().eik_swe_launches(self.h))
 

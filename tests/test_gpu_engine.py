@@ -82,15 +82,6 @@ def test_tighter_tolerance_is_more_accurate(stiff_system):
     assert errs[1] <= errs[0] and errs[0] <= 1e-2 and errs[1] <= 1e-6
 
 
-def test_sparse_and_dense_inputs_agree(stiff_system):
-    import scipy.sparse as sp
-    A, v = stiff_system
-    ref = phipm_simul_iom2(PhiTask(A=A, v=v, rho=[1.0], tol=1e-8)).W
-    for wrapped in (SparseMatrix.from_dense(A), sp.csr_matrix(A)):
-        res = phipm_simul_iom2(PhiTask(A=wrapped, v=v, rho=[1.0], tol=1e-8))
-        assert np.allclose(res.W, ref, rtol=1e-6, atol=1e-10)
-
-
 def test_zero_skip_reduces_matvecs(stiff_system):
     A, v = stiff_system
     n = A.shape[0]
@@ -141,11 +132,73 @@ def test_full_dimension_generic_mgs():
     assert np.max(np.abs(res.W - ref)) <= 1e-9 * np.max(np.abs(ref))
 
 
-def test_callable_operator_rejected(stiff_system):
+def test_engine_accepts_sparse_and_operator_inputs(stiff_system):
+    """test_phipm.py:73-82: SparseMatrix, scipy CSR and a MatvecOperator
+    around a host callable (device engine, one host round trip per matvec)."""
+    import scipy.sparse as sp
     A, v = stiff_system
-    with pytest.raises(TypeError):
-        phipm_simul_iom2(PhiTask(A=MatvecOperator(lambda x: A @ x, 40, A.size), v=v,
-                                 rho=[1.0]))
+    ref = phipm_simul_iom2(PhiTask(A=A, v=v, rho=[1.0], tol=1e-8)).W
+    for wrapped in (SparseMatrix.from_dense(A), sp.csr_matrix(A),
+                    MatvecOperator(lambda x: A @ x, A.shape[0], A.size)):
+        res = phipm_simul_iom2(PhiTask(A=wrapped, v=v, rho=[1.0], tol=1e-8))
+        assert np.allclose(res.W, ref, rtol=1e-6, atol=1e-10)
+
+
+def test_callable_operator_matches_oracle(stiff_system):
+    """The host-callback route: the callable is invoked exactly once per
+    performed matvec (the reference's _CountingOperator count), counters and
+    trace equal the oracle's, W within 1e-9."""
+    from oracle.expint_oracle import OracleOperator
+    A, v = stiff_system
+    seen = []
+
+    def mv(x):
+        seen.append(x.copy())
+        return A @ x
+
+    for rho in ([1.0], [0.3, 0.7, 1.0]):
+        seen.clear()
+        r = phipm_simul_iom2(PhiTask(A=MatvecOperator(mv, 40, A.size), v=v, rho=rho,
+                                     tol=1e-8, trace=True))
+        o = engine_run(OracleOperator(lambda x: A @ x, 40, A.size), v, rho, tol=1e-8,
+                       trace=True)
+        assert len(seen) == r.matvecs
+        assert (r.substeps, r.rejections, r.matvecs, r.m_final) == \
+            (o.substeps, o.rejections, o.matvecs, o.m_final)
+        assert [t[3] for t in r.trace] == [t[3] for t in o.trace]
+        assert np.linalg.norm(r.W - o.W) <= 1e-9 * np.linalg.norm(o.W)
+
+
+def test_callable_operator_exception_propagates(stiff_system):
+    A, v = stiff_system
+    calls = []
+
+    def bad(x):
+        calls.append(1)
+        if len(calls) == 3:
+            raise ZeroDivisionError("boom")
+        return A @ x
+
+    with pytest.raises(ZeroDivisionError):
+        phipm_simul_iom2(PhiTask(A=MatvecOperator(bad, 40, A.size), v=v, rho=[1.0],
+                                 tol=1e-8))
+    assert len(calls) == 3  # no further requests after the failure
+    # the context is reusable afterwards
+    r = phipm_simul_iom2(PhiTask(A=MatvecOperator(lambda x: A @ x, 40, A.size), v=v,
+                                 rho=[1.0], tol=1e-8))
+    assert np.all(np.isfinite(r.W))
+
+
+def test_callable_jacobian_in_integrator_steps():
+    """A problem whose jac returns a MatvecOperator (host callable) steps
+    through the device engine like the SparseMatrix one."""
+    L, problem, u0 = make_linear_problem()
+    hp = SemilinearProblem(n=problem.n, f=problem.f,
+                           jac=lambda u: MatvecOperator(lambda x: L @ x, L.shape[0],
+                                                        int(np.count_nonzero(L))))
+    a = integrate(problem, "exprb42", u0, 0.25, 0.5, tol=1e-10)[-1].u
+    b = integrate(hp, "exprb42", u0, 0.25, 0.5, tol=1e-10)[-1].u
+    assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(a)
 
 
 def make_linear_problem(seed=1, n=24):
