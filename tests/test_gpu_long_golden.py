@@ -105,8 +105,9 @@ def test_c4_l10_runs_conserve_mass():
     steps complete, the state stays finite and the total mass (h weighted by
     cell area) is conserved to 1e-12 (the divergence operator is
     conservative, Df's Laplacian rows sum to zero)."""
-    if os.environ.get("EIK_SKIP_L10"):
-        pytest.skip("EIK_SKIP_L10 set")
+    if not os.environ.get("EIK_RUN_L10"):
+        pytest.skip("L10 run is opt-in (EIK_RUN_L10=1): building the 10.5 M-cell grid "
+                    "takes ~3 min of host time")
     ops, u0, spec = make_config("C4", 10)
     ctx = gswe.context(ops)  # the context diagnostics() reads
     ctx.set_state(u0)
