@@ -478,6 +478,9 @@ struct JvAcc {
 #ifndef EIK_CHUNK
 #define EIK_CHUNK 3
 #endif
+#ifndef EIK_EXP_HALFDV
+#define EIK_EXP_HALFDV 0
+#endif
 // One chunk of CH slots' G/D/V coefficients of own cell i (9 per slot).
 template <int CH>
 struct CoefChunk {
@@ -491,6 +494,10 @@ __device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, Coe
     const double* cp = S.coefc + i + (s0 + k) * st;
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
+#if EIK_EXP_HALFDV
+      // experiment only: D not streamed (V reused) -- wrong results
+      if (q >= 6) { cf.v[k][q] = cf.v[k][q - 6]; continue; }
+#endif
 #if EIK_L2POL
       cf.v[k][q] = ld_stream_pol(cp + q * S.NC, pol_evict_first());
 #else

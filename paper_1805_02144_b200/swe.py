@@ -22,6 +22,68 @@ from .phipm import DeviceOperator, MatvecOperator
 _OP_ORDER = ("Gx", "Gy", "Gz", "Dx", "Dy", "Dz", "Vx", "Vy", "Vz", "L", "Df")
 
 
+def _periodic_diff(n, dx):
+    """Centred periodic first derivative (swe.py:70-76)."""
+    import scipy.sparse as sp
+    e = np.ones(n) / (2.0 * dx)
+    D = sp.diags([e[:-1], -e[:-1]], [1, -1], shape=(n, n), format="lil")
+    D[0, n - 1] = -1.0 / (2.0 * dx)
+    D[n - 1, 0] = 1.0 / (2.0 * dx)
+    return sp.csr_matrix(D)
+
+
+def _periodic_second(n, dx):
+    """Periodic second derivative (swe.py:79-86)."""
+    import scipy.sparse as sp
+    e = np.ones(n) / dx ** 2
+    D = sp.diags([e[:-1], -2.0 * e, e[:-1]], [1, 0, -1], shape=(n, n), format="lil")
+    D[0, n - 1] = 1.0 / dx ** 2
+    D[n - 1, 0] = 1.0 / dx ** 2
+    return sp.csr_matrix(D)
+
+
+def planar_periodic_operators(nx, ny, dx, f0=1e-4, g=9.80616, gamma_h=0.04e-2, h_s=None):
+    """The reference's doubly periodic planar operator set (swe.py:89-121):
+    centred differences, n = z-hat, Vx = -d/dy, Vy = d/dx, Df = -nu L@L.
+    Nodes row-major, index = iy * nx + ix."""
+    import scipy.sparse as sp
+    from .sparse import SparseMatrix
+    if nx < 4 or ny < 4:
+        raise ValueError("grid must be at least 4x4")
+    if dx <= 0.0:
+        raise ValueError("dx must be positive")
+    n_g = nx * ny
+    Ix = sp.identity(nx, format="csr")
+    Iy = sp.identity(ny, format="csr")
+    ddx = sp.kron(Iy, _periodic_diff(nx, dx), format="csr")
+    ddy = sp.kron(_periodic_diff(ny, dx), Ix, format="csr")
+    lap = (sp.kron(Iy, _periodic_second(nx, dx)) + sp.kron(_periodic_second(ny, dx), Ix)).tocsr()
+    zero = sp.csr_matrix((n_g, n_g))
+    nu = dissipation_coefficient(gamma_h, dx)
+    return DiscreteOperators(
+        Gx=SparseMatrix(ddx), Gy=SparseMatrix(ddy), Gz=SparseMatrix(zero),
+        Dx=SparseMatrix(ddx), Dy=SparseMatrix(ddy), Dz=SparseMatrix(zero),
+        Vx=SparseMatrix(-ddy), Vy=SparseMatrix(ddx), Vz=SparseMatrix(zero),
+        L=SparseMatrix(lap), Df=SparseMatrix(-nu * (lap @ lap)),
+        n_x=np.zeros(n_g), n_y=np.zeros(n_g), n_z=np.ones(n_g), f=np.full(n_g, float(f0)),
+        h_s=np.zeros(n_g) if h_s is None else np.asarray(h_s, dtype=float),
+        g=float(g), nu=nu, n_g=n_g, cell_area=dx * dx)
+
+
+def gaussian_hill_state(ops, nx, ny, dx, h0=8000.0, amplitude=100.0, sigma_cells=None,
+                        center=None):
+    """Rest state with a Gaussian bump in the height field (swe.py:240-253)."""
+    if sigma_cells is None:
+        sigma_cells = nx / 8.0
+    if center is None:
+        center = (nx / 2.0, ny / 2.0)
+    X, Y = np.meshgrid(np.arange(nx), np.arange(ny))
+    r2 = (X - center[0]) ** 2 + (Y - center[1]) ** 2
+    h = h0 + amplitude * np.exp(-r2 / (2.0 * sigma_cells ** 2))
+    z = np.zeros(ops.n_g)
+    return stack_state(z, z.copy(), z.copy(), h.ravel())
+
+
 def split_state(ops, state):
     n = ops.n_g
     state = np.asarray(state, dtype=float)
