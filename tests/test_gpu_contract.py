@@ -216,7 +216,7 @@ def test_explicit_orthogonalisation_inside_steps_counted():
 # ------------------------------------------------------ non-tiled path
 
 def _info(ctx):
-    out = (C.c_int64 * 9)()
+    out = (C.c_int64 * 16)()
     nat.check(nat.load().eik_swe_info(ctx.h, out), "info")
     return list(out)
 
