@@ -782,6 +782,31 @@ struct Form {
 #ifndef EIK_REV
 #define EIK_REV 1
 #endif
+// EIK_PF2: prefetch the tile's step-2 rows (E1 neighbour rows + Laplacian
+// rows) into L1 at the start of step 1; EIK_PFT: load the next tile's
+// metadata and prefetch its halo map during step 3 of the current tile
+#ifndef EIK_PF2
+#define EIK_PF2 1
+#endif
+// EIK_PF3: prefetch this tile's coefficient runs (step 3's stream) into L2
+// at the start of step 1 (1) or step 2 (2)
+#ifndef EIK_PF3
+#define EIK_PF3 0
+#endif
+// EIK_PF4: at the start of step 2, prefetch into L1 the own cells' runs that
+// step 3 reads last: (n, eta) and the epilogue's v_{j-1}
+#ifndef EIK_PF4
+#define EIK_PF4 1
+#endif
+#ifndef EIK_PFT
+#define EIK_PFT 0
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
                                           double4 s2) {
@@ -809,15 +834,57 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
   // backwards (alternate Krylov iterations: the tiles written last in one
   // iteration are read first in the next, while their vectors are in L2)
   const int kt = S.ntiles > (int)blockIdx.x ? (S.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile_of = [&](int k) {
+    return (int)blockIdx.x + (EIK_REV && F.rev ? kt - 1 - k : k) * (int)gridDim.x;
+  };
+  struct TileMeta {
+    int64_t c0;
+    int nT, nE1, nE2, e2off, e1off;
+  };
+  auto load_meta = [&](int t) {
+    TileMeta m;
+    m.c0 = __ldg(S.t_cell0 + t);
+    m.nT = __ldg(S.t_nT + t);
+    m.nE1 = __ldg(S.t_nE1 + t);
+    m.nE2 = __ldg(S.t_nE2 + t);
+    m.e2off = __ldg(S.t_e2off + t);
+    m.e1off = __ldg(S.t_e1off + t);
+    return m;
+  };
+  TileMeta nxt;
+  if (EIK_PFT && kt > 0) nxt = load_meta(tile_of(0));
   for (int k = 0; k < kt; ++k) {
-    const int t = (int)blockIdx.x + (EIK_REV && F.rev ? kt - 1 - k : k) * (int)gridDim.x;
-    const int64_t c0 = __ldg(S.t_cell0 + t);
-    const int nT = __ldg(S.t_nT + t), nE1 = __ldg(S.t_nE1 + t), nE2 = __ldg(S.t_nE2 + t);
-    if (nT == 0) continue;  // uniform over the CTA
-    const int* map = S.e2map + __ldg(S.t_e2off + t);
-    const int e1off = __ldg(S.t_e1off + t);
+    const int t = tile_of(k);
+    const TileMeta cur = EIK_PFT ? nxt : load_meta(t);
+    const int64_t c0 = cur.c0;
+    const int nT = cur.nT, nE1 = cur.nE1, nE2 = cur.nE2;
+    if (nT == 0) {  // uniform over the CTA
+      if (EIK_PFT && k + 1 < kt) nxt = load_meta(tile_of(k + 1));
+      continue;
+    }
+    const int* map = S.e2map + cur.e2off;
+    const int e1off = cur.e1off;
     const short* rows = S.lnbr + (int64_t)e1off * 8;
     const double* lce1 = S.LcE1 + (int64_t)e1off * 6;
+    auto pf_coef = [&]() {
+      // 54 runs of nT doubles: [slot][op][NC] from cell c0
+      const int lpr = (nT * 8 + 127) >> 7;  // lines per run (+1 for misalignment)
+      const int per = lpr + 1;
+      for (int q = threadIdx.x; q < NCOEF * per; q += TPB) {
+        const int run = q / per, ln = q - run * per;
+        const char* base = (const char*)(S.coefc + (int64_t)run * S.NC + c0);
+        const char* a = (const char*)((uintptr_t)base & ~(uintptr_t)127) + ((int64_t)ln << 7);
+        if (a < base + nT * 8) prefetch_l2(a);
+      }
+    };
+    if (EIK_PF3 == 1) pf_coef();
+    if (EIK_PF2 && !Step::kE1Only) {
+      // step-2 rows of this tile: nE1 x 16 B (rows) + nE1 x 48 B (Laplacian)
+      const int l1 = (nE1 * 16 + 127) >> 7, l2 = (nE1 * 48 + 127) >> 7;
+      for (int q = threadIdx.x; q < l1 + l2; q += TPB)
+        prefetch_l1(q < l1 ? (const char*)rows + ((int64_t)q << 7)
+                           : (const char*)lce1 + ((int64_t)(q - l1) << 7));
+    }
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
     const int nEs = Step::kE1Only ? nE1 : nE2;  // cells staged in step 1
     for (int base = 0; base < nEs; base += 2 * TPB) {
@@ -864,6 +931,14 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     }
     __syncthreads();
     SRP_MARK(0)
+    if (EIK_PF3 == 2) pf_coef();
+    if (EIK_PF4) {
+      const int ln = (nT * 32 + 127) >> 7;
+      const int nv = F.epi_vm1 ? 2 * ln : ln;
+      for (int q = threadIdx.x; q < nv; q += TPB)
+        prefetch_l1(q < ln ? (const char*)(S.ne + c0) + ((int64_t)q << 7)
+                           : (const char*)(F.epi_vm1 + c0) + ((int64_t)(q - ln) << 7));
+    }
     // step 2: L x on E1 (difference form; rows and coefficients contiguous
     // per tile), two rows per thread per round with their loads issued first
     auto lap_row = [&](int c, const Row8& row, const Lrow& lr) {
@@ -887,6 +962,13 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     }
     SRP_MARK(1)
     // step 3: z = scale * J x on the own cells
+    if (EIK_PFT && k + 1 < kt) {
+      nxt = load_meta(tile_of(k + 1));
+      // the next tile's halo map (nE2 ints) into L2 while step 3 streams
+      const int* nmap = S.e2map + nxt.e2off;
+      const int nl = (nxt.nE2 * 4 + 127) >> 7;
+      for (int q = threadIdx.x; q < nl; q += TPB) prefetch_l2((const char*)nmap + ((int64_t)q << 7));
+    }
     if ((int)threadIdx.x < nT) {
       const int c = threadIdx.x;
       const int64_t i = c0 + c;

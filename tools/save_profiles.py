@@ -66,4 +66,20 @@ if os.path.exists(rep):
                    "cells": 655362, "dram_bytes_per_launch": dram, "krylov_iters_in_launch": iters,
                    "dram_bytes_per_iter": dram / iters},
                   open(os.path.join(dst, "traffic.json"), "w"), indent=1)
+# the continuation and dense kernels (one launch each)
+for kern, stem in (("k_swe_cont", "cont"), ("k_swe_dense", "dense")):
+    rep = os.path.join(src, f"{stem}_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    out = subprocess.run([sys.executable, "tools/ncu_summary.py", rep], capture_output=True, text=True).stdout
+    r = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(io.StringIO(r.stdout)))
+    hdr = rows[0]
+    si, mi, ui, vi = (hdr.index(x) for x in ("Section Name", "Metric Name", "Metric Unit", "Metric Value"))
+    det = [f"{r[si][:30]:30s} {r[mi]:48s} {r[vi]:>16s} {r[ui]}" for r in rows[1:]
+           if r[si] in ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Occupancy",
+                        "Launch Statistics", "Warp State Statistics", "Compute Workload Analysis")]
+    with open(os.path.join(dst, f"ncu_full_{kern}_{tag}.txt"), "w") as fh:
+        fh.write(f"ncu --set full --clock-control none -k regex:{kern} -s 3 -c 1 (host-loop "
+                 f"mode, C3 L8 exprb42 bench steps)\n\n{out}\n\n" + "\n".join(det) + "\n")
 print(sorted(os.listdir(dst)))
