@@ -6,9 +6,11 @@ unmodified reference ``integrate`` / ``phipm_simul_iom2`` run on our sphere
 ``DiscreteOperators`` and seeded states, and the results are stored as small
 .npz fixtures that travel to the GPU box (where /root/reference does not).
 
-    python tests/golden/make_golden.py [--big]
+    python tests/golden/make_golden.py [--big] [--c4]
 
-Writes tests/golden/*.npz.  ``--big`` adds the L7/L8 prefixes (minutes).
+Writes tests/golden/*.npz.  ``--big`` adds the L7/L8 prefixes (minutes),
+``--c4`` the L9 first step.  The full-length runs of every config are made
+by make_long_golden.py.
 """
 
 import hashlib
@@ -106,6 +108,11 @@ def main():
         save("c3_exprb42_1", ops, u0, recs, calls, secs, False)
         recs, calls, secs = run_reference(ops, u0, "epi3", 600.0, 2, 1e-8)
         save("c3_epi3_2", ops, u0, recs, calls, secs, False)
+    if "--c4" in sys.argv:
+        # C4 at L9 (2.6 M cells): the cold-start EXPRB4 step (~210 s here)
+        ops, u0, spec = make_config("C4")
+        recs, calls, secs = run_reference(ops, u0, "exprb42", 900.0, 1, 1e-8)
+        save("c4_exprb42_1", ops, u0, recs, calls, secs, False)
 
 
 if __name__ == "__main__":
