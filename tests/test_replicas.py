@@ -52,3 +52,36 @@ def test_single_process_identity():
     assert max_over_ranks(3.5) == 3.5
     v, ms = aggregate_throughput(4, 200.0)
     assert ms == 200.0 and v == pytest.approx(20.0)
+
+
+def test_bench_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself with two ranks
+    (127.0.0.1 rendezvous); the reference arm prints one line from rank 0
+    with n_gpus = 2 (CPU-only: the reference arm needs no device)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["OMP_NUM_THREADS"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--impl", "reference", "--config", "C0", "--steps", "2",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                       env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_bench_rejects_world_size_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--impl", "reference", "--config", "C0"], capture_output=True,
+                       text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
