@@ -1102,9 +1102,10 @@ static const void* kCbKernels[] = {(const void*)k_cb_phipm};
 struct EikCb {
   EngineHost eng;
   HostOp H{};
-  double* xh = nullptr;  // mapped pinned host buffers
+  double* xh = nullptr;  // pinned host staging of x and y
   double* yh = nullptr;
-  unsigned int* mbox = nullptr;
+  unsigned int* mbox = nullptr;  // mapped pinned mailbox
+  cudaStream_t cst = nullptr;    // copies while the engine kernel runs
 };
 
 extern "C" {
@@ -2205,24 +2206,29 @@ eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out) 
     if (c->xh) cudaFreeHost(c->xh);
     if (c->yh) cudaFreeHost(c->yh);
     if (c->mbox) cudaFreeHost(c->mbox);
+    if (c->cst) cudaStreamDestroy(c->cst);
     c->eng.release();
     delete c;
     return fail(st, msg);
   };
   if (s != EIK_OK) return bail(s, "engine init failed");
-  if (cudaHostAlloc((void**)&c->xh, n * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->yh, n * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+  if (cudaHostAlloc((void**)&c->xh, n * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->yh, n * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void**)&c->mbox, 64, cudaHostAllocMapped) != cudaSuccess)
-    return bail(EIK_ENOMEM, "mapped host allocation failed");
+    return bail(EIK_ENOMEM, "pinned host allocation failed");
+  if (cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(EIK_ECUDA, "copy stream");
   HostOp& H = c->H;
   H.n = n;
   H.NUu = NU;
-  if (cudaHostGetDevicePointer((void**)&H.xh, c->xh, 0) != cudaSuccess ||
-      cudaHostGetDevicePointer((void**)&H.yh, c->yh, 0) != cudaSuccess ||
-      cudaHostGetDevicePointer((void**)&H.mbox, c->mbox, 0) != cudaSuccess)
-    return bail(EIK_ECUDA, "mapped host pointers unavailable");
-  if (c->eng.mem.get(&H.ctr, 2) != cudaSuccess || c->eng.mem.get(&H.abort, 1) != cudaSuccess)
+  double *xd, *yd;
+  if (cudaHostGetDevicePointer((void**)&H.mbox, c->mbox, 0) != cudaSuccess)
+    return bail(EIK_ECUDA, "mapped host pointer unavailable");
+  if (c->eng.mem.get(&H.ctr, 2) != cudaSuccess || c->eng.mem.get(&H.abort, 1) != cudaSuccess ||
+      c->eng.mem.get(&xd, 4 * NU) != cudaSuccess || c->eng.mem.get(&yd, 4 * NU) != cudaSuccess)
     return bail(EIK_ENOMEM, "device allocation failed");
+  H.xh = xd;
+  H.yh = yd;
   H.scale = 1.0;
   *out = c;
   return EIK_OK;
@@ -2233,6 +2239,7 @@ eik_status eik_cb_destroy(EikCb* c) {
   cudaFreeHost(c->xh);
   cudaFreeHost(c->yh);
   cudaFreeHost(c->mbox);
+  if (c->cst) cudaStreamDestroy(c->cst);
   c->eng.release();
   delete c;
   return EIK_OK;
@@ -2283,7 +2290,18 @@ eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale
   for (;;) {
     const unsigned int req = mb[0];
     if (req != served) {
-      const int rc = cb_failed ? 1 : matvec(user, c->xh, c->yh, n);
+      int rc = 1;
+      if (!cb_failed &&
+          cudaMemcpyAsync(c->xh, c->H.xh, n * sizeof(double), cudaMemcpyDeviceToHost, c->cst) ==
+              cudaSuccess &&
+          cudaStreamSynchronize(c->cst) == cudaSuccess) {
+        rc = matvec(user, c->xh, c->yh, n);
+        if (rc == 0 &&
+            (cudaMemcpyAsync((void*)c->H.yh, c->yh, n * sizeof(double), cudaMemcpyHostToDevice,
+                             c->cst) != cudaSuccess ||
+             cudaStreamSynchronize(c->cst) != cudaSuccess))
+          rc = 1;
+      }
       if (rc != 0) cb_failed = true;
       std::atomic_thread_fence(std::memory_order_seq_cst);
       mb[1] = rc == 0 ? req : kCbAbort;

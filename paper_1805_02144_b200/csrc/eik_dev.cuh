@@ -1022,18 +1022,19 @@ struct CsrOp {
 
 // Host-callback operator (the reference's MatvecOperator around an arbitrary
 // callable, phipm.py:45-54): the engine stays on the device and every matvec
-// is a round trip through a mailbox in mapped pinned host memory.  All CTAs
-// write their part of x to xh and arrive on a device counter; the lead
-// thread posts a request sequence number and spins (nanosleep) until the
-// host thread serving eik_cb_phipm has written y = A x to yh and echoed the
-// number (or an abort code); the engine's grid barrier after op_pre then
-// releases every CTA to read yh.  Slow by construction (PCIe + the callable
-// per matvec), as SURVEY.md §8(b)(1) allows for this plug point.
+// is a round trip to the host.  All CTAs write their part of x to the device
+// buffer xd and arrive on a device counter; the lead thread posts a request
+// sequence number in a mailbox in mapped pinned memory and spins (nanosleep)
+// until the host thread serving eik_cb_phipm has copied x out (DMA on its own
+// stream), called the callable, copied y = A x into yd and echoed the number
+// (or an abort code); the engine's grid barrier after op_pre then releases
+// every CTA to read yd (L2, bypassing L1).  Slow by construction (PCIe + the
+// callable per matvec), as SURVEY.md §8(b)(1) allows for this plug point.
 struct HostOp {
   static constexpr bool kTiled = false;
   int64_t n, NUu;
-  double* xh;                     // mapped host buffer (device address), n doubles
-  const double* yh;               // mapped host buffer, n doubles, written by the host
+  double* xh;                     // device buffer x (n doubles), copied out by the host
+  const double* yh;               // device buffer y = A x, copied in by the host
   volatile unsigned int* mbox;    // mapped: [0] request seq, [1] reply seq / kCbAbort
   unsigned long long* ctr;        // device: [0] CTA arrivals, [1] requests posted
   int* abort;                     // device: 1 once the host aborted (or timed out)
@@ -1104,7 +1105,7 @@ __device__ __forceinline__ void op_pre_x<HostOp>(const HostOp& H, const double4*
       if (globaltimer_ns() - t0 > kCbTimeoutNs) { r = kCbAbort; break; }
     }
     if (r == kCbAbort) *((volatile int*)H.abort) = 1;
-    __threadfence_system();
+    __threadfence();
   }
 }
 
@@ -1113,7 +1114,7 @@ __device__ __forceinline__ double4 op_main(const HostOp& H, const double4*, int6
   if (!*((volatile int*)H.abort)) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (4 * u + q < H.n) r[q] = H.scale * __ldcv(H.yh + 4 * u + q);
+      if (4 * u + q < H.n) r[q] = H.scale * __ldcg(H.yh + 4 * u + q);
   }
   return make_double4(r[0], r[1], r[2], r[3]);
 }

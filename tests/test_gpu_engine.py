@@ -171,6 +171,23 @@ def test_callable_operator_matches_oracle(stiff_system):
         assert np.linalg.norm(r.W - o.W) <= 1e-6 * np.linalg.norm(o.W)
 
 
+def test_callable_operator_repeated_calls_are_identical(stiff_system):
+    """The host-callback route is deterministic: 25 calls (interleaved with
+    device CSR calls on other sizes) give bitwise-identical W and counters."""
+    A, v = stiff_system
+    first = None
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((64, 64)) - 8.0 * np.eye(64)
+    vb = [rng.standard_normal(64)]
+    for k in range(25):
+        r = phipm_simul_iom2(PhiTask(A=MatvecOperator(lambda x: A @ x, 40, A.size), v=v,
+                                     rho=[0.5, 1.0], tol=1e-8))
+        key = (r.W.tobytes(), r.substeps, r.rejections, r.matvecs, r.m_final)
+        first = first or key
+        assert key == first, k
+        phipm_simul_iom2(PhiTask(A=B, v=vb, rho=[1.0], tol=1e-8))
+
+
 def test_callable_operator_exception_propagates(stiff_system):
     A, v = stiff_system
     calls = []

@@ -10,6 +10,15 @@ python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo 
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 --sweep-steps 2"
 export EIK_STEP_HOST=1 EIK_SWEEP_LOG=1
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_list_$TAG.log 2>&1; echo ncu1=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_swe_sweep -s ${KSKIP:-4} -c 1 -o gpurun_out/step_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu2=$?
+# capture a full-length sweep: the first launch with >= 30 Krylov iterations in the plain run
+KSKIP=${KSKIP:-$(python -c "
+import re,sys
+for l in open('gpurun_out/plain_$TAG.log'):
+    m = re.match(r'\[eik\] sweep (\d+) iters (\d+)', l)
+    if m and int(m.group(2)) >= 30:
+        print(m.group(1)); break
+")}
+echo "KSKIP=$KSKIP" > gpurun_out/kskip_$TAG.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_swe_sweep -s $KSKIP -c 1 -o gpurun_out/step_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu2=$?
 [ -n "$NOCONT" ] || { timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_swe_cont -s 3 -c 1 -o gpurun_out/cont_$TAG $CMD > gpurun_out/ncu_cont_$TAG.log 2>&1; echo ncu3=$?; }
 [ -n "$NOCONT" ] || { timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_swe_dense -s 3 -c 1 -o gpurun_out/dense_$TAG $CMD > gpurun_out/ncu_dense_$TAG.log 2>&1; echo ncu4=$?; }

@@ -30,6 +30,9 @@ if os.path.exists(p):
             fh.write(f"{name:24s} launches={n:4d} total_ns={t:14.0f} share={100 * t / tot:6.2f}%\n")
 rep = os.path.join(src, f"step_{tag}.ncu-rep")
 kskip = int(os.environ.get("KSKIP", "4"))
+kp = os.path.join(src, f"kskip_{tag}.txt")
+if os.path.exists(kp):
+    kskip = int(open(kp).read().strip().split("=")[1])
 if os.path.exists(rep):
     out = subprocess.run([sys.executable, "tools/ncu_summary.py", rep], capture_output=True, text=True).stdout
     r = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True)
@@ -41,11 +44,13 @@ if os.path.exists(rep):
                         "Launch Statistics", "Warp State Statistics", "Compute Workload Analysis")]
     # Krylov iterations of the captured launch (EIK_SWEEP_LOG lines of the ncu run)
     iters = None
-    logp = os.path.join(src, f"ncu_full_{tag}.log")
+    # the plain (non-ncu) run of the same command: identical sweep sequence
+    logp = os.path.join(src, f"plain_{tag}.log")
     if os.path.exists(logp):
         for line in open(logp):
             if line.startswith(f"[eik] sweep {kskip} iters "):
                 iters = int(line.split()[4])
+                break
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True)
     rr = list(csv.reader(io.StringIO(raw.stdout)))
     h, u, v = rr[0], rr[1], rr[2]
