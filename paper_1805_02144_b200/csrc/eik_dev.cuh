@@ -481,6 +481,17 @@ struct JvAcc {
 #ifndef EIK_EXP_HALFDV
 #define EIK_EXP_HALFDV 0
 #endif
+// EIK_PRE3: the Krylov pass issues step 3's first coefficient chunk before
+// the barrier that ends step 2 (the loads fly while the CTA's last rows finish)
+#ifndef EIK_PRE3
+#define EIK_PRE3 0
+#endif
+// EIK_BAR1: the barrier that ends a tile is taken inside the next tile's
+// step 1, after its gathers are issued and before its first shared-memory
+// store (a warp that finishes step 3 early starts the next tile's gathers)
+#ifndef EIK_BAR1
+#define EIK_BAR1 0
+#endif
 // One chunk of CH slots' G/D/V coefficients of own cell i (9 per slot).
 template <int CH>
 struct CoefChunk {
@@ -557,21 +568,29 @@ __device__ __forceinline__ void jv_accum(const SweOp& S, const TileSmem& ts, con
 // are issued before any of them is used (a compiler memory fence keeps them
 // together), so each thread keeps ~27 streaming loads in flight instead of
 // the handful the default schedule interleaves with the math.
+constexpr int JCH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
+using JvChunk = CoefChunk<JCH>;
+template <bool PRE>
 __device__ __forceinline__ JvAcc swe_jv_sum(const SweOp& S, const TileSmem& ts, const short* row,
                                             const double* lc, int64_t i, double4 ai, double4 Ui,
-                                            double4 lai) {
+                                            double4 lai, const JvChunk& pre) {
   const JvOwn o = jv_own(S, ai, Ui, lai);
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  constexpr int CH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
+  constexpr int CH = JCH;
 #pragma unroll
   for (int k0 = 0; k0 < KCMAX; k0 += CH) {
     CoefChunk<CH> cf;
-    coef_load<CH>(S, i, k0, cf);
-    asm volatile("" ::: "memory");
+    if (PRE && k0 == 0) {
+      cf = pre;  // issued by the caller before the step-2 barrier
+    } else {
+      coef_load<CH>(S, i, k0, cf);
+      asm volatile("" ::: "memory");
+    }
     jv_accum<CH>(S, ts, row, lc, k0, cf, o, a);
   }
   return a;
 }
+
 
 __device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a, double4 q,
                                                  double4 ai, double4 Ui) {
@@ -597,10 +616,13 @@ __device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a,
 struct JvStep {
   static constexpr bool kStageHs = false;
   static constexpr bool kE1Only = false;
+  static constexpr bool kPre3 = EIK_PRE3 != 0;
+  static constexpr bool kIsJv = true;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
-                                                double4 ai, double4 Ui, double4 lai) const {
-    const JvAcc a = swe_jv_sum(S, ts, row, lc, i, ai, Ui, lai);
+                                                double4 ai, double4 Ui, double4 lai,
+                                                const JvChunk& pre) const {
+    const JvAcc a = swe_jv_sum<kPre3>(S, ts, row, lc, i, ai, Ui, lai, pre);
     return S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
   }
 };
@@ -652,6 +674,8 @@ __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, co
 struct RhsStep {
   static constexpr bool kStageHs = true;
   static constexpr bool kE1Only = false;
+  static constexpr bool kPre3 = false;
+  static constexpr bool kIsJv = false;
   bool write_ne;  // store (n, eta) of every own cell to S.ne (linearisation at w)
   bool write_gn;  // store g_n = F*(w) - J*(w) w to S.gn (for DevStep)
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
@@ -705,6 +729,8 @@ struct RhsStep {
 struct DevStep {
   static constexpr bool kStageHs = false;
   static constexpr bool kE1Only = true;
+  static constexpr bool kPre3 = false;
+  static constexpr bool kIsJv = false;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* /*lc*/,
                                                 int64_t i, double4 Ui, double4 li,
@@ -800,6 +826,10 @@ struct Form {
 #endif
 #ifndef EIK_PFT
 #define EIK_PFT 0
+#endif
+// EIK_HALF2: step 2 works on half rows (see there)
+#ifndef EIK_HALF2
+#define EIK_HALF2 0
 #endif
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -910,6 +940,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
           ub = Step::kStageHs ? make_double4(__ldg(S.hs + gb), 0.0, 0.0, 0.0)
                                 : ldv_nc(S.lin + gb);
       }
+      if (EIK_BAR1 && base == 0 && k > 0) __syncthreads();  // previous tile's step 3 done
       if (va) {
         const double4 x = form_x(F, a0, a1, a2);
         sst(ts.x, ca, x);
@@ -955,9 +986,36 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       }
       sst(ts.La, c, acc);
     };
+    [[maybe_unused]] JvChunk pre3;
     if (!Step::kE1Only) {
+#if EIK_HALF2 && EIK_SPLIT
+      // half rows: task t < nE1 is the (x, y) half of row t, t >= nE1 the (z, w)
+      // half of row t - nE1 (the two halves live in separate shared arrays), so
+      // the 2 * nE1 tasks balance over the CTA better than nE1 whole rows
+      for (int t = threadIdx.x; t < 2 * nE1; t += TPB) {
+        const int hh = t >= nE1 ? 1 : 0;
+        const int c = t - hh * nE1;
+        const Row8 row = load_row8(rows + (int64_t)c * 8);
+        const Lrow lr = load_lrow(lce1 + (int64_t)c * 6);
+        const double2* xp = ts.x.p + hh * ts.x.n;
+        const double2 xc = xp[c];
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < KCMAX; ++s) {
+          const double l = lr.v[s];
+          const double2 xv = xp[row.s[s]];
+          acc.x += l * (xv.x - xc.x);
+          acc.y += l * (xv.y - xc.y);
+        }
+        ts.La.p[hh * ts.La.n + c] = acc;
+      }
+#else
       for (int c = threadIdx.x; c < nE1; c += TPB)
         lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
+#endif
+      if constexpr (Step::kPre3) {
+        if ((int)threadIdx.x < nT) coef_load<JCH>(S, c0 + threadIdx.x, 0, pre3);
+      }
       __syncthreads();
     }
     SRP_MARK(1)
@@ -977,13 +1035,17 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       const double4 lai = Step::kE1Only ? d4(0.0) : sld(ts.La, c);
       const Row8 row = load_row8(rows + (int64_t)c * 8);
       const Lrow lr = Step::kE1Only ? Lrow{} : load_lrow(lce1 + (int64_t)c * 6);
-      const double4 z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
+      double4 z;
+      if constexpr (Step::kIsJv) z = step(S, ts, row.s, lr.v, i, ai, Ui, lai, pre3);
+      else z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
     }
-    __syncthreads();
+    // the tile's shared arrays are rewritten by the next tile's step 1
+    if (!EIK_BAR1) __syncthreads();
     SRP_MARK(2)
   }
+  if (EIK_BAR1) __syncthreads();
 #if EIK_PROF
   if (S.prof && threadIdx.x == 0) {
     for (int k = 0; k < 3; ++k) atomicAdd(S.prof + k, (unsigned long long)pst[k]);
