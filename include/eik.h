@@ -230,7 +230,14 @@ eik_status eik_csr_phipm(EikCsr* ctx, double scale, int64_t nnz_override,
  * writes y = A x (n doubles, both host memory owned by the context), returns
  * 0 on success; any other value aborts the call with EIK_ECALLBACK.  It is
  * invoked on the thread that called eik_cb_phipm, once per performed matvec
- * (zero-skipped products are not requested), in the engine's order. */
+ * (zero-skipped products are not requested), in the engine's order.
+ * While the call runs, the engine's cooperative kernel holds every SM and
+ * waits for the host, so the callable must be host code: a libeik entry
+ * point called from inside it fails with EIK_EINVAL, eik_*_destroy calls made
+ * meanwhile (finalisers, a garbage collector) are deferred until the call
+ * returns, and a request left unanswered for EIK_CB_TIMEOUT_S seconds
+ * (environment, default 600) -- e.g. because the callable made a call that
+ * synchronises the device -- ends the call with EIK_ECALLBACK. */
 typedef int (*eik_matvec_fn)(void* user, const double* x, double* y, int64_t n);
 typedef struct EikCb EikCb;
 eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out);

@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <functional>
 #include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -21,6 +23,36 @@ using namespace eik;
 
 // ====================================================================== errors
 static thread_local std::string g_err;
+
+// While a host-callback engine (eik_cb_phipm) is running, its cooperative
+// kernel occupies every SM and waits for the host: a device-synchronising
+// call made meanwhile (cudaFree in a destroy run by a finaliser or garbage
+// collector inside the callable) would wait for that kernel and deadlock.
+// Destroys are therefore deferred until the engine call has finished, and
+// libeik entry points called from inside the callable fail with EIK_EINVAL.
+static std::atomic<int> g_cb_inflight{0};
+static thread_local bool g_in_callback = false;
+static std::mutex g_defer_mu;
+static std::vector<std::function<void()>> g_deferred;
+#define EIK_NO_REENTRY()                                                                   \
+  if (g_in_callback)                                                                       \
+  return fail(EIK_EINVAL, "libeik called from inside a matvec callback (the device engine " \
+                          "is waiting for it)")
+static bool defer_destroy(std::function<void()> fn) {
+  std::lock_guard<std::mutex> lk(g_defer_mu);
+  if (g_cb_inflight.load() == 0) return false;
+  g_deferred.push_back(std::move(fn));
+  return true;
+}
+static void drain_deferred() {
+  std::vector<std::function<void()>> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_defer_mu);
+    if (g_cb_inflight.load() != 0) return;
+    todo.swap(g_deferred);
+  }
+  for (auto& f : todo) f();
+}
 #ifndef EIK_LPT
 #define EIK_LPT 0
 #endif
@@ -1129,6 +1161,7 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
                           const double* n_y, const double* n_z, const double* f,
                           const double* h_s, double g, double nu, int32_t device,
                           int32_t m_max, EikSwe** out) {
+  EIK_NO_REENTRY();
   if (!out || !ops || n_g < 1 || !n_x || !n_y || !n_z || !f || !h_s)
     return fail(EIK_EINVAL, "invalid arguments to eik_swe_create");
   const int64_t N = n_g;
@@ -1587,8 +1620,14 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   return EIK_OK;
 }
 
+static void swe_destroy_now(EikSwe* c);
 eik_status eik_swe_destroy(EikSwe* c) {
   if (!c) return EIK_OK;
+  if (defer_destroy([c] { swe_destroy_now(c); })) return EIK_OK;
+  swe_destroy_now(c);
+  return EIK_OK;
+}
+static void swe_destroy_now(EikSwe* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1596,10 +1635,10 @@ eik_status eik_swe_destroy(EikSwe* c) {
   if (c->evs1) cudaEventDestroy(c->evs1);
   c->eng.release();
   delete c;
-  return EIK_OK;
 }
 
 eik_status eik_swe_set_state(EikSwe* c, const double* u) {
+  EIK_NO_REENTRY();
   if (!c || !u) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->u);
@@ -1609,12 +1648,14 @@ eik_status eik_swe_set_state(EikSwe* c, const double* u) {
 }
 
 eik_status eik_swe_get_state(EikSwe* c, double* u) {
+  EIK_NO_REENTRY();
   if (!c || !u) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   return c->d2h_cells(c->u, u);
 }
 
 eik_status eik_swe_set_prev(EikSwe* c, const double* u_prev) {
+  EIK_NO_REENTRY();
   if (!c) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   if (!u_prev) {
@@ -1629,6 +1670,7 @@ eik_status eik_swe_set_prev(EikSwe* c, const double* u_prev) {
 }
 
 eik_status eik_swe_rhs(EikSwe* c, const double* u, double* out) {
+  EIK_NO_REENTRY();
   if (!c || !u || !out) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
@@ -1640,6 +1682,7 @@ eik_status eik_swe_rhs(EikSwe* c, const double* u, double* out) {
 }
 
 eik_status eik_swe_jv(EikSwe* c, const double* u, const double* v, double* out) {
+  EIK_NO_REENTRY();
   if (!c || !u || !v || !out) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
@@ -1653,6 +1696,7 @@ eik_status eik_swe_jv(EikSwe* c, const double* u, const double* v, double* out) 
 
 eik_status eik_swe_jac_nnz_rows(EikSwe* c, const double* u, int64_t* nnz,
                                 double* per_cell) {
+  EIK_NO_REENTRY();
   if (!c || !u || !nnz) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
@@ -1673,6 +1717,7 @@ eik_status eik_swe_jac_nnz_rows(EikSwe* c, const double* u, int64_t* nnz,
 }
 
 eik_status eik_swe_jac_nnz(EikSwe* c, const double* u, int64_t* nnz) {
+  EIK_NO_REENTRY();
   if (!c || !u || !nnz) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = c->h2d_cells(u, c->x);
@@ -1689,6 +1734,7 @@ eik_status eik_swe_jac_nnz(EikSwe* c, const double* u, int64_t* nnz) {
 eik_status eik_swe_phipm(EikSwe* c, const double* u_lin, double dt,
                          const EikPhiTask* task, double* W, EikPhipmInfo* info,
                          EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  EIK_NO_REENTRY();
   if (!c || !u_lin || !W) return fail(EIK_EINVAL, "invalid arguments");
   EngineHost& E = c->eng;
   if (task && task->m_max > E.m_alloc) {
@@ -1883,6 +1929,7 @@ static eik_status step_enqueue(EikSwe* c, int32_t scheme, double dt, double tol)
 
 eik_status eik_swe_step(EikSwe* c, int32_t scheme, double dt, double tol,
                         EikPhipmInfo* calls, int32_t* ncalls) {
+  EIK_NO_REENTRY();
   if (!c) return fail(EIK_EINVAL, "invalid arguments");
   if (!(dt > 0.0)) return fail(EIK_EINVAL, "dt must be positive");
   if (scheme < 0 || scheme > EIK_EXPRB53) return fail(EIK_EINVAL, "unknown scheme");
@@ -1907,6 +1954,7 @@ eik_status eik_swe_step(EikSwe* c, int32_t scheme, double dt, double tol,
 
 eik_status eik_swe_advance(EikSwe* c, int32_t scheme, double dt, double tol,
                            int32_t nsteps, int64_t* matvecs, int64_t* substeps) {
+  EIK_NO_REENTRY();
   if (!c || nsteps < 0) return fail(EIK_EINVAL, "invalid arguments");
   if (scheme == EIK_EPI3 && !c->have_prev)
     return fail(EIK_EINVAL, "epi3 requires the previous state");
@@ -1950,6 +1998,7 @@ eik_status eik_swe_reset_seeds(EikSwe* c) {
 }
 
 eik_status eik_swe_snapshot(EikSwe* c, int32_t restore) {
+  EIK_NO_REENTRY();
   if (!c) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   const size_t vb = (size_t)c->N * sizeof(double4), sb = 2 * EIK_NUM_SLOTS * sizeof(double);
@@ -1977,6 +2026,7 @@ eik_status eik_swe_snapshot(EikSwe* c, int32_t restore) {
 
 eik_status eik_swe_krylov_bench(EikSwe* c, const double* u, const double* v, double dt,
                                 int32_t m, int32_t reps, double* out) {
+  EIK_NO_REENTRY();
   if (!c || !u || !v || !out || m < 1 || reps < 1) return fail(EIK_EINVAL, "invalid arguments");
   if (m > c->eng.m_alloc) return fail(EIK_EINVAL, "m exceeds the basis allocation");
   CK(cudaSetDevice(c->eng.dev));
@@ -2006,6 +2056,7 @@ eik_status eik_swe_krylov_bench(EikSwe* c, const double* u, const double* v, dou
 
 eik_status eik_swe_diagnostics(EikSwe* c, const double* u, const double* weights,
                                double cell_area, double* out) {
+  EIK_NO_REENTRY();
   if (!c || !out) return fail(EIK_EINVAL, "invalid arguments");
   CK(cudaSetDevice(c->eng.dev));
   eik_status s = EIK_OK;
@@ -2108,6 +2159,7 @@ int64_t eik_swe_explicit_orth(const EikSwe* c) {
 // ------------------------------------------------------------------ CSR
 eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max,
                           EikCsr** out) {
+  EIK_NO_REENTRY();
   if (!out || n < 1 || !A.indptr || A.indptr[n] != A.nnz)
     return fail(EIK_EINVAL, "invalid CSR operator");
   for (int64_t k = 0; k < A.nnz; ++k) {
@@ -2147,14 +2199,18 @@ eik_status eik_csr_create(int32_t n, EikCsrView A, int32_t device, int32_t m_max
 
 eik_status eik_csr_destroy(EikCsr* c) {
   if (!c) return EIK_OK;
-  c->eng.release();
-  delete c;
+  auto now = [c] {
+    c->eng.release();
+    delete c;
+  };
+  if (!defer_destroy(now)) now();
   return EIK_OK;
 }
 
 eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
                          const EikPhiTask* task, double* W, EikPhipmInfo* info,
                          EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  EIK_NO_REENTRY();
   if (!c || !W) return fail(EIK_EINVAL, "invalid arguments");
   EngineHost& E = c->eng;
   if (task && task->m_max > E.m_alloc) {
@@ -2196,6 +2252,7 @@ eik_status eik_csr_phipm(EikCsr* c, double scale, int64_t nnz_override,
 
 // ------------------------------------------------- host-callback operator
 eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out) {
+  EIK_NO_REENTRY();
   if (!out || n < 1) return fail(EIK_EINVAL, "invalid arguments");
   EikCb* c = new EikCb();
   const int64_t NU = (n + 3) / 4;
@@ -2236,18 +2293,22 @@ eik_status eik_cb_create(int64_t n, int32_t device, int32_t m_max, EikCb** out) 
 
 eik_status eik_cb_destroy(EikCb* c) {
   if (!c) return EIK_OK;
-  cudaFreeHost(c->xh);
-  cudaFreeHost(c->yh);
-  cudaFreeHost(c->mbox);
-  if (c->cst) cudaStreamDestroy(c->cst);
-  c->eng.release();
-  delete c;
+  auto now = [c] {
+    cudaFreeHost(c->xh);
+    cudaFreeHost(c->yh);
+    cudaFreeHost(c->mbox);
+    if (c->cst) cudaStreamDestroy(c->cst);
+    c->eng.release();
+    delete c;
+  };
+  if (!defer_destroy(now)) now();
   return EIK_OK;
 }
 
 eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale, int64_t nnz,
                         const EikPhiTask* task, double* W, EikPhipmInfo* info,
                         EikTraceRec* trace, int64_t trace_cap, int64_t* trace_len) {
+  EIK_NO_REENTRY();
   if (!c || !W || !matvec) return fail(EIK_EINVAL, "invalid arguments");
   EngineHost& E = c->eng;
   if (task && task->m_max > E.m_alloc) {
@@ -2269,6 +2330,11 @@ eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale
   memset(&A, 0, sizeof(A));
   A.H = c->H;
   A.H.scale = scale;
+  A.H.timeout_ns = kCbTimeoutNs;
+  if (const char* e = getenv("EIK_CB_TIMEOUT_S")) {
+    const double sec = atof(e);
+    if (sec > 0.0) A.H.timeout_ns = (unsigned long long)(sec * 1e9);
+  }
   A.Wk = E.wk;
   A.Wk.nnz = nnz;
   A.Wk.trace = (trace && trace_cap > 0) ? E.trace_d : nullptr;
@@ -2282,6 +2348,14 @@ eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale
   CK(cudaMemsetAsync(c->H.abort, 0, sizeof(int), E.st));
   CK(cudaMemsetAsync(E.trace_len_d, 0, sizeof(int64_t), E.st));
   void* kargs[] = {&A};
+  // destroys requested while the engine waits for the host are deferred (see g_cb_inflight)
+  struct Inflight {
+    Inflight() { ++g_cb_inflight; }
+    ~Inflight() {
+      --g_cb_inflight;
+      drain_deferred();
+    }
+  } inflight;
   CK(cudaLaunchCooperativeKernel((const void*)k_cb_phipm, E.G, TPB, kargs, E.smem, E.st));
   ++E.launches;
   // serve the kernel's matvec requests until it finishes
@@ -2295,7 +2369,9 @@ eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale
           cudaMemcpyAsync(c->xh, c->H.xh, n * sizeof(double), cudaMemcpyDeviceToHost, c->cst) ==
               cudaSuccess &&
           cudaStreamSynchronize(c->cst) == cudaSuccess) {
+        g_in_callback = true;
         rc = matvec(user, c->xh, c->yh, n);
+        g_in_callback = false;
         if (rc == 0 &&
             (cudaMemcpyAsync((void*)c->H.yh, c->yh, n * sizeof(double), cudaMemcpyHostToDevice,
                              c->cst) != cudaSuccess ||
@@ -2314,6 +2390,13 @@ eik_status eik_cb_phipm(EikCb* c, eik_matvec_fn matvec, void* user, double scale
   }
   s = E.finish_phipm(info, trace, trace_cap, trace_len);
   if (cb_failed) return fail(EIK_ECALLBACK, "matvec callback failed");
+  // a request the host did not answer in time aborts the engine on the device
+  // side; an attempt already under way may still have completed on zero products
+  int aborted = 0;
+  CK(cudaMemcpy(&aborted, c->H.abort, sizeof(int), cudaMemcpyDeviceToHost));
+  if (aborted)
+    return fail(EIK_ECALLBACK, "matvec request timed out: the host did not answer (a call that "
+                               "synchronises the device inside the callable?)");
   if (s != EIK_OK) return s;
   for (int i = 0; i < task->ns; ++i)
     CK(cudaMemcpyAsync(W + (size_t)i * n, E.wout[i], n * sizeof(double), cudaMemcpyDeviceToHost, E.st));

@@ -481,16 +481,29 @@ struct JvAcc {
 #ifndef EIK_EXP_HALFDV
 #define EIK_EXP_HALFDV 0
 #endif
-// EIK_PRE3: the Krylov pass issues step 3's first coefficient chunk before
-// the barrier that ends step 2 (the loads fly while the CTA's last rows finish)
-#ifndef EIK_PRE3
-#define EIK_PRE3 0
+// EIK_SMETA: tile metadata staged in shared memory 16 tiles at a time;
+// EIK_PFM (with it): the next tile's halo map prefetched into L1 during step 3
+#ifndef EIK_SMETA
+#define EIK_SMETA 0
+#endif
+#ifndef EIK_PFM
+#define EIK_PFM 0
+#endif
+// EIK_ROW0: every thread loads row threadIdx.x of the tile's step-2 rows
+// before the barrier that ends step 1 and keeps it for step 3 (own cells)
+#ifndef EIK_ROW0
+#define EIK_ROW0 0
+#endif
+// EIK_PF5: L2 prefetch of step 3's first coefficient chunk just before the
+// barrier that ends step 2
+#ifndef EIK_PF5
+#define EIK_PF5 0
 #endif
 // EIK_BAR1: the barrier that ends a tile is taken inside the next tile's
 // step 1, after its gathers are issued and before its first shared-memory
 // store (a warp that finishes step 3 early starts the next tile's gathers)
 #ifndef EIK_BAR1
-#define EIK_BAR1 0
+#define EIK_BAR1 1
 #endif
 // One chunk of CH slots' G/D/V coefficients of own cell i (9 per slot).
 template <int CH>
@@ -570,22 +583,17 @@ __device__ __forceinline__ void jv_accum(const SweOp& S, const TileSmem& ts, con
 // the handful the default schedule interleaves with the math.
 constexpr int JCH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
 using JvChunk = CoefChunk<JCH>;
-template <bool PRE>
 __device__ __forceinline__ JvAcc swe_jv_sum(const SweOp& S, const TileSmem& ts, const short* row,
                                             const double* lc, int64_t i, double4 ai, double4 Ui,
-                                            double4 lai, const JvChunk& pre) {
+                                            double4 lai) {
   const JvOwn o = jv_own(S, ai, Ui, lai);
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   constexpr int CH = JCH;
 #pragma unroll
   for (int k0 = 0; k0 < KCMAX; k0 += CH) {
     CoefChunk<CH> cf;
-    if (PRE && k0 == 0) {
-      cf = pre;  // issued by the caller before the step-2 barrier
-    } else {
-      coef_load<CH>(S, i, k0, cf);
-      asm volatile("" ::: "memory");
-    }
+    coef_load<CH>(S, i, k0, cf);
+    asm volatile("" ::: "memory");
     jv_accum<CH>(S, ts, row, lc, k0, cf, o, a);
   }
   return a;
@@ -616,13 +624,10 @@ __device__ __forceinline__ double4 swe_jv_finish(const SweOp& S, const JvAcc& a,
 struct JvStep {
   static constexpr bool kStageHs = false;
   static constexpr bool kE1Only = false;
-  static constexpr bool kPre3 = EIK_PRE3 != 0;
-  static constexpr bool kIsJv = true;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
-                                                double4 ai, double4 Ui, double4 lai,
-                                                const JvChunk& pre) const {
-    const JvAcc a = swe_jv_sum<kPre3>(S, ts, row, lc, i, ai, Ui, lai, pre);
+                                                double4 ai, double4 Ui, double4 lai) const {
+    const JvAcc a = swe_jv_sum(S, ts, row, lc, i, ai, Ui, lai);
     return S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
   }
 };
@@ -674,8 +679,6 @@ __device__ __forceinline__ void rhs_accum(const SweOp& S, const TileSmem& ts, co
 struct RhsStep {
   static constexpr bool kStageHs = true;
   static constexpr bool kE1Only = false;
-  static constexpr bool kPre3 = false;
-  static constexpr bool kIsJv = false;
   bool write_ne;  // store (n, eta) of every own cell to S.ne (linearisation at w)
   bool write_gn;  // store g_n = F*(w) - J*(w) w to S.gn (for DevStep)
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
@@ -729,8 +732,6 @@ struct RhsStep {
 struct DevStep {
   static constexpr bool kStageHs = false;
   static constexpr bool kE1Only = true;
-  static constexpr bool kPre3 = false;
-  static constexpr bool kIsJv = false;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* /*lc*/,
                                                 int64_t i, double4 Ui, double4 li,
@@ -827,10 +828,6 @@ struct Form {
 #ifndef EIK_PFT
 #define EIK_PFT 0
 #endif
-// EIK_HALF2: step 2 works on half rows (see there)
-#ifndef EIK_HALF2
-#define EIK_HALF2 0
-#endif
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -883,9 +880,37 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
   };
   TileMeta nxt;
   if (EIK_PFT && kt > 0) nxt = load_meta(tile_of(0));
+#if EIK_SMETA
+  // the metadata of this CTA's next SMW tiles, staged in shared memory by one
+  // thread per tile (one round trip per SMW tiles instead of one per tile)
+  constexpr int SMW = 16;
+  __shared__ int s_meta[SMW][6];
+  auto smeta = [&](int k) {
+    const int* m = s_meta[k % SMW];
+    return TileMeta{m[0], m[1], m[2], m[3], m[4], m[5]};
+  };
+#endif
   for (int k = 0; k < kt; ++k) {
     const int t = tile_of(k);
+#if EIK_SMETA
+    if (k % SMW == 0) {
+      if (k) __syncthreads();  // every warp has read the previous window
+      if ((int)threadIdx.x < SMW && k + (int)threadIdx.x < kt) {
+        const int tt = tile_of(k + threadIdx.x);
+        int* m = s_meta[threadIdx.x];
+        m[0] = __ldg(S.t_cell0 + tt);
+        m[1] = __ldg(S.t_nT + tt);
+        m[2] = __ldg(S.t_nE1 + tt);
+        m[3] = __ldg(S.t_nE2 + tt);
+        m[4] = __ldg(S.t_e2off + tt);
+        m[5] = __ldg(S.t_e1off + tt);
+      }
+      __syncthreads();
+    }
+    const TileMeta cur = smeta(k);
+#else
     const TileMeta cur = EIK_PFT ? nxt : load_meta(t);
+#endif
     const int64_t c0 = cur.c0;
     const int nT = cur.nT, nE1 = cur.nE1, nE2 = cur.nE2;
     if (nT == 0) {  // uniform over the CTA
@@ -960,6 +985,15 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
         }
       }
     }
+    // row threadIdx.x of the tile: step 2's first row and, for an own cell, step 3's
+    // (EIK_ROW0: loaded before the barrier that ends step 1 and kept)
+    Row8 row0;
+    Lrow lr0;
+    const bool has0 = (int)threadIdx.x < nE1;
+    if (EIK_ROW0 && has0) {
+      row0 = load_row8(rows + (int64_t)threadIdx.x * 8);
+      if (!Step::kE1Only) lr0 = load_lrow(lce1 + (int64_t)threadIdx.x * 6);
+    }
     __syncthreads();
     SRP_MARK(0)
     if (EIK_PF3 == 2) pf_coef();
@@ -986,35 +1020,20 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       }
       sst(ts.La, c, acc);
     };
-    [[maybe_unused]] JvChunk pre3;
     if (!Step::kE1Only) {
-#if EIK_HALF2 && EIK_SPLIT
-      // half rows: task t < nE1 is the (x, y) half of row t, t >= nE1 the (z, w)
-      // half of row t - nE1 (the two halves live in separate shared arrays), so
-      // the 2 * nE1 tasks balance over the CTA better than nE1 whole rows
-      for (int t = threadIdx.x; t < 2 * nE1; t += TPB) {
-        const int hh = t >= nE1 ? 1 : 0;
-        const int c = t - hh * nE1;
-        const Row8 row = load_row8(rows + (int64_t)c * 8);
-        const Lrow lr = load_lrow(lce1 + (int64_t)c * 6);
-        const double2* xp = ts.x.p + hh * ts.x.n;
-        const double2 xc = xp[c];
-        double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int s = 0; s < KCMAX; ++s) {
-          const double l = lr.v[s];
-          const double2 xv = xp[row.s[s]];
-          acc.x += l * (xv.x - xc.x);
-          acc.y += l * (xv.y - xc.y);
-        }
-        ts.La.p[hh * ts.La.n + c] = acc;
+      if (EIK_ROW0) {
+        if (has0) lap_row(threadIdx.x, row0, lr0);
+        for (int c = threadIdx.x + TPB; c < nE1; c += TPB)
+          lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
+      } else {
+        for (int c = threadIdx.x; c < nE1; c += TPB)
+          lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
       }
-#else
-      for (int c = threadIdx.x; c < nE1; c += TPB)
-        lap_row(c, load_row8(rows + (int64_t)c * 8), load_lrow(lce1 + (int64_t)c * 6));
-#endif
-      if constexpr (Step::kPre3) {
-        if ((int)threadIdx.x < nT) coef_load<JCH>(S, c0 + threadIdx.x, 0, pre3);
+      if (EIK_PF5 && (int)threadIdx.x < nT) {
+        // step 3's first coefficient chunk into L2 while the CTA's last rows finish
+        const double* cp = S.coefc + c0 + threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < 9 * JCH; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
       }
       __syncthreads();
     }
@@ -1027,17 +1046,25 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       const int nl = (nxt.nE2 * 4 + 127) >> 7;
       for (int q = threadIdx.x; q < nl; q += TPB) prefetch_l2((const char*)nmap + ((int64_t)q << 7));
     }
+#if EIK_SMETA && EIK_PFM
+    if (k + 1 < kt && (k + 1) % SMW != 0) {
+      // the next tile's halo map into L1 while step 3 streams
+      const TileMeta nm = smeta(k + 1);
+      const int nl = ((Step::kE1Only ? nm.nE1 : nm.nE2) * 4 + 127) >> 7;
+      if ((int)threadIdx.x < nl)
+        prefetch_l1((const char*)(S.e2map + nm.e2off) + ((int64_t)threadIdx.x << 7));
+    }
+#endif
     if ((int)threadIdx.x < nT) {
       const int c = threadIdx.x;
       const int64_t i = c0 + c;
       const double4 ai = sld(ts.x, c);
       const double4 Ui = sld(ts.U, c);
       const double4 lai = Step::kE1Only ? d4(0.0) : sld(ts.La, c);
-      const Row8 row = load_row8(rows + (int64_t)c * 8);
-      const Lrow lr = Step::kE1Only ? Lrow{} : load_lrow(lce1 + (int64_t)c * 6);
-      double4 z;
-      if constexpr (Step::kIsJv) z = step(S, ts, row.s, lr.v, i, ai, Ui, lai, pre3);
-      else z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
+      const Row8 row = EIK_ROW0 ? row0 : load_row8(rows + (int64_t)c * 8);
+      const Lrow lr = Step::kE1Only ? Lrow{}
+                                    : (EIK_ROW0 ? lr0 : load_lrow(lce1 + (int64_t)c * 6));
+      const double4 z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
     }
@@ -1100,11 +1127,12 @@ struct HostOp {
   volatile unsigned int* mbox;    // mapped: [0] request seq, [1] reply seq / kCbAbort
   unsigned long long* ctr;        // device: [0] CTA arrivals, [1] requests posted
   int* abort;                     // device: 1 once the host aborted (or timed out)
+  unsigned long long timeout_ns;  // a request unanswered for this long aborts the call
   double scale;
   __device__ __forceinline__ int64_t NU() const { return NUu; }
 };
 constexpr unsigned int kCbAbort = 0xFFFFFFFFu;
-constexpr unsigned long long kCbTimeoutNs = 600ull * 1000000000ull;
+constexpr unsigned long long kCbTimeoutNs = 600ull * 1000000000ull;  // default (EIK_CB_TIMEOUT_S)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -1164,7 +1192,7 @@ __device__ __forceinline__ void op_pre_x<HostOp>(const HostOp& H, const double4*
     unsigned int r;
     while ((r = H.mbox[1]) != seq && r != kCbAbort) {
       __nanosleep(2000);
-      if (globaltimer_ns() - t0 > kCbTimeoutNs) { r = kCbAbort; break; }
+      if (globaltimer_ns() - t0 > H.timeout_ns) { r = kCbAbort; break; }
     }
     if (r == kCbAbort) *((volatile int*)H.abort) = 1;
     __threadfence();

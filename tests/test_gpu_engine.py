@@ -208,6 +208,61 @@ def test_callable_operator_exception_propagates(stiff_system):
     assert np.all(np.isfinite(r.W))
 
 
+def test_context_finalised_inside_callable_is_deferred(stiff_system, monkeypatch):
+    """A device context destroyed while the host-callback engine waits for the
+    host (a garbage collector running inside the callable) must not touch the
+    device: cudaFree would wait for the engine's kernel, which waits for the
+    host.  libeik defers such destroys until the call returns; a libeik call
+    from inside the callable is an error."""
+    import ctypes as C
+    import gc
+    import scipy.sparse as sp
+    from paper_1805_02144_b200 import _native as nat
+    monkeypatch.setenv("EIK_CB_TIMEOUT_S", "30")
+    A, v = stiff_system
+    ref = phipm_simul_iom2(PhiTask(A=A, v=v, rho=[1.0], tol=1e-8))
+
+    class Holder:
+        pass
+
+    def make_garbage():
+        csr = sp.csr_matrix(A)
+        view, keep = nat.csr_view(csr)
+        h = C.c_void_p()
+        nat.check(nat.load().eik_csr_create(40, view, 0, 40, C.byref(h)), "eik_csr_create")
+        hold = Holder()
+        hold.me = hold  # a reference cycle: freed by the collector only
+        hold.ctx = phipm_mod._CsrCtx(h)
+
+    gc.collect()
+    gc.disable()
+    try:
+        make_garbage()
+        calls = []
+
+        def mv(x):
+            if not calls:
+                gc.collect()  # runs _CsrCtx.__del__ -> eik_csr_destroy
+            calls.append(1)
+            return A @ x
+
+        r = phipm_simul_iom2(PhiTask(A=MatvecOperator(mv, 40, A.size), v=v, rho=[1.0],
+                                     tol=1e-8))
+    finally:
+        gc.enable()
+    assert (r.substeps, r.rejections, r.matvecs, r.m_final) == \
+        (ref.substeps, ref.rejections, ref.matvecs, ref.m_final)
+    assert np.allclose(r.W, ref.W, rtol=1e-6, atol=1e-10)
+
+    def reentrant(x):
+        phipm_simul_iom2(PhiTask(A=A, v=v, rho=[1.0], tol=1e-8))
+        return A @ x
+
+    with pytest.raises(ValueError, match="inside a matvec callback"):
+        phipm_simul_iom2(PhiTask(A=MatvecOperator(reentrant, 40, A.size), v=v, rho=[1.0],
+                                 tol=1e-8))
+
+
 def test_callable_jacobian_in_integrator_steps():
     """A problem whose jac returns a MatvecOperator (host callable) steps
     through the device engine like the SparseMatrix one."""
