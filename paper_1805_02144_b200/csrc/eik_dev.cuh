@@ -153,6 +153,13 @@ __device__ __forceinline__ double ld_stream_pol(const double* p, uint64_t pol) {
   return v;
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ---------------------------------------------------------------- shared
 struct Smem {
   double red[NWARP][NPART];
@@ -484,11 +491,21 @@ struct JvAcc {
 // EIK_SMETA: tile metadata staged in shared memory 16 tiles at a time;
 // EIK_PFM (with it): the next tile's halo map prefetched into L1 during step 3
 #ifndef EIK_SMETA
-#define EIK_SMETA 0
+#define EIK_SMETA 1
 #endif
 #ifndef EIK_PFM
-#define EIK_PFM 0
+#define EIK_PFM 1
 #endif
+// EIK_PF6: step 3 prefetches the next coefficient chunk into L2 right after
+// issuing the current chunk's loads
+#ifndef EIK_PF6
+#define EIK_PF6 0
+#endif
+// unroll factor of the candidate's sum over the basis vectors (loads in flight)
+#ifndef EIK_CANDU
+#define EIK_CANDU 4
+#endif
+constexpr int kCandU = EIK_CANDU;
 // EIK_ROW0: every thread loads row threadIdx.x of the tile's step-2 rows
 // before the barrier that ends step 1 and keeps it for step 3 (own cells)
 #ifndef EIK_ROW0
@@ -497,7 +514,15 @@ struct JvAcc {
 // EIK_PF5: L2 prefetch of step 3's first coefficient chunk just before the
 // barrier that ends step 2
 #ifndef EIK_PF5
-#define EIK_PF5 0
+#define EIK_PF5 1
+#endif
+// runs [0, EIK_PF5A) are prefetched at the start of step 2, runs
+// [EIK_PF5A, EIK_PF5A + EIK_PF5N) at its end (27 runs = the first chunk)
+#ifndef EIK_PF5A
+#define EIK_PF5A 0
+#endif
+#ifndef EIK_PF5N
+#define EIK_PF5N 27
 #endif
 // EIK_BAR1: the barrier that ends a tile is taken inside the next tile's
 // step 1, after its gathers are issued and before its first shared-memory
@@ -593,6 +618,12 @@ __device__ __forceinline__ JvAcc swe_jv_sum(const SweOp& S, const TileSmem& ts, 
   for (int k0 = 0; k0 < KCMAX; k0 += CH) {
     CoefChunk<CH> cf;
     coef_load<CH>(S, i, k0, cf);
+    if (EIK_PF6 && k0 + CH < KCMAX) {
+      // the next chunk into L2 behind this one
+      const double* cp = S.coefc + i + (int64_t)(k0 + CH) * 9 * S.NC;
+#pragma unroll
+      for (int q = 0; q < 9 * CH; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
+    }
     asm volatile("" ::: "memory");
     jv_accum<CH>(S, ts, row, lc, k0, cf, o, a);
   }
@@ -828,12 +859,6 @@ struct Form {
 #ifndef EIK_PFT
 #define EIK_PFT 0
 #endif
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
                                           double4 s2) {
@@ -1021,6 +1046,11 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       sst(ts.La, c, acc);
     };
     if (!Step::kE1Only) {
+      if (EIK_PF5 && EIK_PF5A > 0 && (int)threadIdx.x < nT) {
+        const double* cp = S.coefc + c0 + threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < EIK_PF5A && q < NCOEF; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
+      }
       if (EIK_ROW0) {
         if (has0) lap_row(threadIdx.x, row0, lr0);
         for (int c = threadIdx.x + TPB; c < nE1; c += TPB)
@@ -1033,7 +1063,8 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
         // step 3's first coefficient chunk into L2 while the CTA's last rows finish
         const double* cp = S.coefc + c0 + threadIdx.x;
 #pragma unroll
-        for (int q = 0; q < 9 * JCH; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
+        for (int q = EIK_PF5A; q < EIK_PF5A + EIK_PF5N && q < NCOEF; ++q)
+          prefetch_l2(cp + (int64_t)q * S.NC);
       }
       __syncthreads();
     }
@@ -2137,6 +2168,7 @@ __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
       }
       if (wp_nz) {
         double4 s = d4(0.0);
+#pragma unroll kCandU
         for (int64_t k = 0; k < keep; ++k) s = s + sm.phi[k] * Wk.basis[k * NU + u];
         double4 ap = beta * s;
         if (!broke) {
