@@ -161,12 +161,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 // ---------------------------------------------------------------- shared
+constexpr int SMW = 16;  // tiles of metadata staged at a time
 struct Smem {
   double red[NWARP][NPART];
   double tot[NPART];
   double phi[MAXDIM + 4];
   int ival[4];
   int par;      // partial-buffer parity (double buffering, see grid_reduce)
+  int meta[SMW][6];  // tiled pass: metadata of the CTA's next SMW tiles
 };
 
 __device__ __forceinline__ void brange(int64_t NU, int64_t& lo, int64_t& hi) {
@@ -868,6 +870,28 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
   return div4(x, f.h);
 }
 
+// this CTA's tiles are t = blockIdx.x + k * gridDim.x, k < tile_count; rev walks
+// them backwards (alternate Krylov iterations: the tiles written last in one
+// iteration are read first in the next, while their vectors are in L2)
+__device__ __forceinline__ int tile_count(const SweOp& S) {
+  return S.ntiles > (int)blockIdx.x ? (S.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+}
+__device__ __forceinline__ int tile_index(int k, int kt, int rev) {
+  return (int)blockIdx.x + (EIK_REV && rev ? kt - 1 - k : k) * (int)gridDim.x;
+}
+// metadata of tiles [k, k + SMW) of the walk into sm.meta (one thread per tile)
+__device__ __forceinline__ void tile_meta_fill(Smem& sm, const SweOp& S, int k, int kt, int rev) {
+  if ((int)threadIdx.x < SMW && k + (int)threadIdx.x < kt) {
+    const int tt = tile_index(k + threadIdx.x, kt, rev);
+    int* m = sm.meta[threadIdx.x];
+    m[0] = __ldg(S.t_cell0 + tt);
+    m[1] = __ldg(S.t_nT + tt);
+    m[2] = __ldg(S.t_nE1 + tt);
+    m[3] = __ldg(S.t_nE2 + tt);
+    m[4] = __ldg(S.t_e2off + tt);
+    m[5] = __ldg(S.t_e1off + tt);
+  }
+}
 // One pass over every tile: x on E2 -> smem, L x on E1, z = scale * J x on
 // the own cells -> epi(i, z, x_i, epi_vm1_i).  A whole Krylov iteration
 // (orthogonalise + normalise v_j, L v_j, J v_j, projections) is one such
@@ -882,13 +906,8 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
 #else
 #define SRP_MARK(k)
 #endif
-  // this CTA's tiles are t = blockIdx.x + k * gridDim.x; F.rev walks them
-  // backwards (alternate Krylov iterations: the tiles written last in one
-  // iteration are read first in the next, while their vectors are in L2)
-  const int kt = S.ntiles > (int)blockIdx.x ? (S.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  auto tile_of = [&](int k) {
-    return (int)blockIdx.x + (EIK_REV && F.rev ? kt - 1 - k : k) * (int)gridDim.x;
-  };
+  const int kt = tile_count(S);
+  auto tile_of = [&](int k) { return tile_index(k, kt, F.rev); };
   struct TileMeta {
     int64_t c0;
     int nT, nE1, nE2, e2off, e1off;
@@ -908,10 +927,8 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
 #if EIK_SMETA
   // the metadata of this CTA's next SMW tiles, staged in shared memory by one
   // thread per tile (one round trip per SMW tiles instead of one per tile)
-  constexpr int SMW = 16;
-  __shared__ int s_meta[SMW][6];
   auto smeta = [&](int k) {
-    const int* m = s_meta[k % SMW];
+    const int* m = sm.meta[k % SMW];
     return TileMeta{m[0], m[1], m[2], m[3], m[4], m[5]};
   };
 #endif
@@ -920,16 +937,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
 #if EIK_SMETA
     if (k % SMW == 0) {
       if (k) __syncthreads();  // every warp has read the previous window
-      if ((int)threadIdx.x < SMW && k + (int)threadIdx.x < kt) {
-        const int tt = tile_of(k + threadIdx.x);
-        int* m = s_meta[threadIdx.x];
-        m[0] = __ldg(S.t_cell0 + tt);
-        m[1] = __ldg(S.t_nT + tt);
-        m[2] = __ldg(S.t_nE1 + tt);
-        m[3] = __ldg(S.t_nE2 + tt);
-        m[4] = __ldg(S.t_e2off + tt);
-        m[5] = __ldg(S.t_e1off + tt);
-      }
+      tile_meta_fill(sm, S, k, kt, F.rev);
       __syncthreads();
     }
     const TileMeta cur = smeta(k);
