@@ -196,7 +196,7 @@ __host__ __device__ constexpr int part_stride(int G) { return (G + 31) & ~31; }
 
 template <int NV>
 __device__ void grid_reduce(cg::grid_group& grid, Smem& sm, double (&v)[NV], double* part) {
-  static_assert(NV <= NWARP && NV <= NPART, "one warp per reduced value");
+  static_assert(NV <= NPART && NV <= TPB, "partials per CTA");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = gridDim.x, Gp = part_stride(G);
   const int par = sm.par;
@@ -215,8 +215,9 @@ __device__ void grid_reduce(cg::grid_group& grid, Smem& sm, double (&v)[NV], dou
   }
   if (threadIdx.x == 0) sm.par = par ^ 1;
   grid.sync();
-  if (w < NV) {
-    const double* row = P + (int64_t)w * Gp;
+  // one warp per reduced value (round robin when a CTA has fewer warps)
+  for (int k = w; k < NV; k += NWARP) {
+    const double* row = P + (int64_t)k * Gp;
     double s = 0.0;
     for (int b0 = 0; b0 < G; b0 += 32 * 8) {
       double x[8];
@@ -228,7 +229,7 @@ __device__ void grid_reduce(cg::grid_group& grid, Smem& sm, double (&v)[NV], dou
       s += ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
     }
     s = warp_sum(s);
-    if (lane == 0) sm.tot[w] = s;
+    if (lane == 0) sm.tot[k] = s;
   }
   __syncthreads();
 #pragma unroll
