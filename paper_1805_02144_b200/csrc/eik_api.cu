@@ -1288,7 +1288,11 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   int NT = 0;
   {
     std::vector<int32_t> mark(N, -1);
-    for (int64_t per = (N + (int64_t)Gt * TILE - 1) / ((int64_t)Gt * TILE);; ++per) {
+    // tiles per CTA: the fewest that keep every tile within TILE cells and the
+    // shared-memory budget; EIK_TILES_EXTRA (environment, experiments) adds to it
+    int64_t per0 = (N + (int64_t)Gt * TILE - 1) / ((int64_t)Gt * TILE);
+    if (const char* e = getenv("EIK_TILES_EXTRA")) per0 += std::max(0, atoi(e));
+    for (int64_t per = per0;; ++per) {
       NT = (int)(Gt * per);
       for (int64_t i = 0; i < N; ++i) ord[i] = (int32_t)i;
       tstart.clear();
