@@ -1486,6 +1486,33 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
     t_e2off.swap(e2b);
     t_e1off.swap(e1b);
   }
+  // tile-major coefficient blocks: each tile's 54 runs contiguous (run stride
+  // nT rounded up to 16 doubles, so every run starts on a 128-byte line) instead
+  // of 54 global runs of N: a tile streams one ~100 KB block, not 54 2-KB pieces
+  // 5 MB apart.  EIK_TILECOEF=0 (environment) keeps the global runs.
+  bool tilecoef = !EIK_LPT;
+  if (const char* e = getenv("EIK_TILECOEF")) tilecoef = tilecoef && atoi(e) != 0;
+  std::vector<int32_t> t_coff(NTb, 0);
+  if (tilecoef) {
+    size_t tot = 0;
+    for (int t = 0; t < NTb; ++t) {
+      t_coff[t] = (int32_t)(tot / 16);
+      tot += (size_t)NCOEF * ((t_nT[t] + 15) & ~15);
+    }
+    if (tot / 16 > (size_t)INT32_MAX) {
+      tilecoef = false;
+    } else {
+      std::vector<double> blk(tot + 16, 0.0);
+      for (int t = 0; t < NTb; ++t) {
+        const size_t cs = (size_t)((t_nT[t] + 15) & ~15), b0 = (size_t)t_coff[t] * 16;
+        for (int r = 0; r < NCOEF; ++r)
+          for (int cc = 0; cc < t_nT[t]; ++cc)
+            blk[b0 + r * cs + cc] = coefc[(size_t)r * NC + t_cell0[t] + cc];
+      }
+      coefc.swap(blk);
+    }
+    if (!tilecoef) std::fill(t_coff.begin(), t_coff.end(), 0);
+  }
   EikSwe* c = new EikSwe();
   c->N = N;
   c->K = K;
@@ -1546,6 +1573,9 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   CKC(cudaMemcpy(d_tnE2, t_nE2.data(), NTb * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_te2, t_e2off.data(), NTb * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_te1, t_e1off.data(), NTb * 4, cudaMemcpyHostToDevice));
+  int* d_tcoff;
+  CKC(B.get(&d_tcoff, NTb));
+  CKC(cudaMemcpy(d_tcoff, t_coff.data(), NTb * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_e2map, e2map.data(), e2map.size() * 4, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_lnbr, lnbr.data(), lnbr.size() * 2, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(d_Lc, Lc.data(), Lc.size() * 8, cudaMemcpyHostToDevice));
@@ -1610,6 +1640,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   S.Lc = d_Lc;
   S.coefc = d_coefc;
   S.NC = NC;
+  S.t_coff = d_tcoff;
+  S.tilecoef = tilecoef ? 1 : 0;
   S.LcE1 = d_LcE1;
   S.KC = KC;
   S.tiled_ok = tiled_ok ? 1 : 0;

@@ -168,7 +168,7 @@ struct Smem {
   double phi[MAXDIM + 4];
   int ival[4];
   int par;      // partial-buffer parity (double buffering, see grid_reduce)
-  int meta[SMW][6];  // tiled pass: metadata of the CTA's next SMW tiles
+  int meta[SMW][7];  // tiled pass: metadata of the CTA's next SMW tiles
 };
 
 __device__ __forceinline__ void brange(int64_t NU, int64_t& lo, int64_t& hi) {
@@ -269,8 +269,12 @@ struct SweOp {
   const int* t_e1off;    // offset into lnbr (rows)
   const int* e2map;      // local -> global cell id, order [own, H1, H2]
   const short* lnbr;     // [rows][8] local off-diagonal neighbours of E1 cells
-  const double* coefc;   // [KC][9][NC] off-diagonal G, D, V (compact stencil)
-  int64_t NC;            // coefficient run stride (N rounded up to even: 16-byte runs)
+  const double* coefc;   // off-diagonal G, D, V (compact stencil), 54 runs (slot-major) per
+                         // tile: tile-major blocks [tile][54][pad16(nT)] at t_coff * 16
+                         // (tilecoef), or global runs [54][NC]
+  int64_t NC;            // global run stride (N rounded up to even)
+  const int* t_coff;     // per tile: block offset / 16 doubles (0 for global runs)
+  int tilecoef;
   const double* Lc;      // [N][8] off-diagonal Laplacian row (cell-major)
   const double* LcE1;    // [sum of tile E1][6] Laplacian rows of every tile's E1 cells
                          // in local order (offset t_e1off * 6)
@@ -499,11 +503,6 @@ struct JvAcc {
 #ifndef EIK_PFM
 #define EIK_PFM 1
 #endif
-// EIK_PF6: step 3 prefetches the next coefficient chunk into L2 right after
-// issuing the current chunk's loads
-#ifndef EIK_PF6
-#define EIK_PF6 0
-#endif
 // unroll factor of the candidate's sum over the basis vectors (loads in flight)
 #ifndef EIK_CANDU
 #define EIK_CANDU 4
@@ -538,12 +537,17 @@ template <int CH>
 struct CoefChunk {
   double v[CH][9];
 };
+// cptr: the cell's entry of run 0, cs: run stride (doubles)
+struct CoefPtr {
+  const double* p;
+  int64_t cs;
+};
 template <int CH>
-__device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, CoefChunk<CH>& cf) {
-  const int64_t st = (int64_t)9 * S.NC;
+__device__ __forceinline__ void coef_load(const CoefPtr& C, int s0, CoefChunk<CH>& cf) {
+  const int64_t st = (int64_t)9 * C.cs;
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
-    const double* cp = S.coefc + i + (s0 + k) * st;
+    const double* cp = C.p + (s0 + k) * st;
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
 #if EIK_EXP_HALFDV
@@ -551,9 +555,9 @@ __device__ __forceinline__ void coef_load(const SweOp& S, int64_t i, int s0, Coe
       if (q >= 6) { cf.v[k][q] = cf.v[k][q - 6]; continue; }
 #endif
 #if EIK_L2POL
-      cf.v[k][q] = ld_stream_pol(cp + q * S.NC, pol_evict_first());
+      cf.v[k][q] = ld_stream_pol(cp + q * C.cs, pol_evict_first());
 #else
-      cf.v[k][q] = __ldcs(cp + q * S.NC);
+      cf.v[k][q] = __ldcs(cp + q * C.cs);
 #endif
     }
   }
@@ -612,21 +616,15 @@ __device__ __forceinline__ void jv_accum(const SweOp& S, const TileSmem& ts, con
 constexpr int JCH = (EIK_CHUNK < KCMAX) ? EIK_CHUNK : KCMAX;
 using JvChunk = CoefChunk<JCH>;
 __device__ __forceinline__ JvAcc swe_jv_sum(const SweOp& S, const TileSmem& ts, const short* row,
-                                            const double* lc, int64_t i, double4 ai, double4 Ui,
-                                            double4 lai) {
+                                            const double* lc, const CoefPtr& C, double4 ai,
+                                            double4 Ui, double4 lai) {
   const JvOwn o = jv_own(S, ai, Ui, lai);
   JvAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   constexpr int CH = JCH;
 #pragma unroll
   for (int k0 = 0; k0 < KCMAX; k0 += CH) {
     CoefChunk<CH> cf;
-    coef_load<CH>(S, i, k0, cf);
-    if (EIK_PF6 && k0 + CH < KCMAX) {
-      // the next chunk into L2 behind this one
-      const double* cp = S.coefc + i + (int64_t)(k0 + CH) * 9 * S.NC;
-#pragma unroll
-      for (int q = 0; q < 9 * CH; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
-    }
+    coef_load<CH>(C, k0, cf);
     asm volatile("" ::: "memory");
     jv_accum<CH>(S, ts, row, lc, k0, cf, o, a);
   }
@@ -660,8 +658,9 @@ struct JvStep {
   static constexpr bool kE1Only = false;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
-                                                double4 ai, double4 Ui, double4 lai) const {
-    const JvAcc a = swe_jv_sum(S, ts, row, lc, i, ai, Ui, lai);
+                                                const CoefPtr& C, double4 ai, double4 Ui,
+                                                double4 lai) const {
+    const JvAcc a = swe_jv_sum(S, ts, row, lc, C, ai, Ui, lai);
     return S.scale * swe_jv_finish(S, a, ldv(S.ne + i), ai, Ui);
   }
 };
@@ -717,7 +716,8 @@ struct RhsStep {
   bool write_gn;  // store g_n = F*(w) - J*(w) w to S.gn (for DevStep)
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* lc, int64_t i,
-                                                double4 wi, double4 hsi4, double4 lai) const {
+                                                const CoefPtr& C, double4 wi, double4 hsi4,
+                                                double4 lai) const {
     const double Ei = 0.5 * (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * wi.w;
     const double Hi = S.g * hsi4.x;
     const double Ji = (wi.x * wi.x + wi.y * wi.y + wi.z * wi.z) + S.g * wi.w;
@@ -726,7 +726,7 @@ struct RhsStep {
 #pragma unroll
     for (int k0 = 0; k0 < KCMAX; k0 += CH) {
       CoefChunk<CH> cf;
-      coef_load<CH>(S, i, k0, cf);
+      coef_load<CH>(C, k0, cf);
       asm volatile("" ::: "memory");
       rhs_accum<CH>(S, ts, row, lc, k0, cf, wi, Ei, Hi, Ji, lai, a);
     }
@@ -768,8 +768,8 @@ struct DevStep {
   static constexpr bool kE1Only = true;
   __device__ __forceinline__ double4 operator()(const SweOp& S, const TileSmem& ts,
                                                 const short* row, const double* /*lc*/,
-                                                int64_t i, double4 Ui, double4 li,
-                                                double4 /*lai*/) const {
+                                                int64_t i, const CoefPtr& C, double4 Ui,
+                                                double4 li, double4 /*lai*/) const {
     const double Ei = 0.5 * (Ui.x * Ui.x + Ui.y * Ui.y + Ui.z * Ui.z) + S.g * Ui.w;
     const double ei = li.x * Ui.x + li.y * Ui.y + li.z * Ui.z + S.g * Ui.w;
     const double fxi = Ui.x * Ui.w, fyi = Ui.y * Ui.w, fzi = Ui.z * Ui.w;
@@ -781,7 +781,7 @@ struct DevStep {
 #pragma unroll
     for (int k0 = 0; k0 < KCMAX; k0 += CH) {
       CoefChunk<CH> cf;
-      coef_load<CH>(S, i, k0, cf);
+      coef_load<CH>(C, k0, cf);
       asm volatile("" ::: "memory");
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
@@ -849,11 +849,6 @@ struct Form {
 #ifndef EIK_PF2
 #define EIK_PF2 1
 #endif
-// EIK_PF3: prefetch this tile's coefficient runs (step 3's stream) into L2
-// at the start of step 1 (1) or step 2 (2)
-#ifndef EIK_PF3
-#define EIK_PF3 0
-#endif
 // EIK_PF4: at the start of step 2, prefetch into L1 the own cells' runs that
 // step 3 reads last: (n, eta) and the epilogue's v_{j-1}
 #ifndef EIK_PF4
@@ -891,6 +886,7 @@ __device__ __forceinline__ void tile_meta_fill(Smem& sm, const SweOp& S, int k, 
     m[3] = __ldg(S.t_nE2 + tt);
     m[4] = __ldg(S.t_e2off + tt);
     m[5] = __ldg(S.t_e1off + tt);
+    m[6] = __ldg(S.t_coff + tt);
   }
 }
 // One pass over every tile: x on E2 -> smem, L x on E1, z = scale * J x on
@@ -911,7 +907,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
   auto tile_of = [&](int k) { return tile_index(k, kt, F.rev); };
   struct TileMeta {
     int64_t c0;
-    int nT, nE1, nE2, e2off, e1off;
+    int nT, nE1, nE2, e2off, e1off, coff;
   };
   auto load_meta = [&](int t) {
     TileMeta m;
@@ -921,6 +917,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     m.nE2 = __ldg(S.t_nE2 + t);
     m.e2off = __ldg(S.t_e2off + t);
     m.e1off = __ldg(S.t_e1off + t);
+    m.coff = __ldg(S.t_coff + t);
     return m;
   };
   TileMeta nxt;
@@ -930,7 +927,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
   // thread per tile (one round trip per SMW tiles instead of one per tile)
   auto smeta = [&](int k) {
     const int* m = sm.meta[k % SMW];
-    return TileMeta{m[0], m[1], m[2], m[3], m[4], m[5]};
+    return TileMeta{m[0], m[1], m[2], m[3], m[4], m[5], m[6]};
   };
 #endif
   for (int k = 0; k < kt; ++k) {
@@ -955,18 +952,9 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     const int e1off = cur.e1off;
     const short* rows = S.lnbr + (int64_t)e1off * 8;
     const double* lce1 = S.LcE1 + (int64_t)e1off * 6;
-    auto pf_coef = [&]() {
-      // 54 runs of nT doubles: [slot][op][NC] from cell c0
-      const int lpr = (nT * 8 + 127) >> 7;  // lines per run (+1 for misalignment)
-      const int per = lpr + 1;
-      for (int q = threadIdx.x; q < NCOEF * per; q += TPB) {
-        const int run = q / per, ln = q - run * per;
-        const char* base = (const char*)(S.coefc + (int64_t)run * S.NC + c0);
-        const char* a = (const char*)((uintptr_t)base & ~(uintptr_t)127) + ((int64_t)ln << 7);
-        if (a < base + nT * 8) prefetch_l2(a);
-      }
-    };
-    if (EIK_PF3 == 1) pf_coef();
+    // the tile's 54 coefficient runs: entry of own cell c at ctile + c, run stride cstr
+    const double* ctile = S.tilecoef ? S.coefc + (int64_t)cur.coff * 16 : S.coefc + c0;
+    const int64_t cstr = S.tilecoef ? (int64_t)((nT + 15) & ~15) : S.NC;
     if (EIK_PF2 && !Step::kE1Only) {
       // step-2 rows of this tile: nE1 x 16 B (rows) + nE1 x 48 B (Laplacian)
       const int l1 = (nE1 * 16 + 127) >> 7, l2 = (nE1 * 48 + 127) >> 7;
@@ -1030,7 +1018,6 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     }
     __syncthreads();
     SRP_MARK(0)
-    if (EIK_PF3 == 2) pf_coef();
     if (EIK_PF4) {
       const int ln = (nT * 32 + 127) >> 7;
       const int nv = F.epi_vm1 ? 2 * ln : ln;
@@ -1056,9 +1043,9 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     };
     if (!Step::kE1Only) {
       if (EIK_PF5 && EIK_PF5A > 0 && (int)threadIdx.x < nT) {
-        const double* cp = S.coefc + c0 + threadIdx.x;
+        const double* cp = ctile + threadIdx.x;
 #pragma unroll
-        for (int q = 0; q < EIK_PF5A && q < NCOEF; ++q) prefetch_l2(cp + (int64_t)q * S.NC);
+        for (int q = 0; q < EIK_PF5A && q < NCOEF; ++q) prefetch_l2(cp + (int64_t)q * cstr);
       }
       if (EIK_ROW0) {
         if (has0) lap_row(threadIdx.x, row0, lr0);
@@ -1070,10 +1057,10 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       }
       if (EIK_PF5 && (int)threadIdx.x < nT) {
         // step 3's first coefficient chunk into L2 while the CTA's last rows finish
-        const double* cp = S.coefc + c0 + threadIdx.x;
+        const double* cp = ctile + threadIdx.x;
 #pragma unroll
         for (int q = EIK_PF5A; q < EIK_PF5A + EIK_PF5N && q < NCOEF; ++q)
-          prefetch_l2(cp + (int64_t)q * S.NC);
+          prefetch_l2(cp + (int64_t)q * cstr);
       }
       __syncthreads();
     }
@@ -1104,7 +1091,7 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
       const Row8 row = EIK_ROW0 ? row0 : load_row8(rows + (int64_t)c * 8);
       const Lrow lr = Step::kE1Only ? Lrow{}
                                     : (EIK_ROW0 ? lr0 : load_lrow(lce1 + (int64_t)c * 6));
-      const double4 z = step(S, ts, row.s, lr.v, i, ai, Ui, lai);
+      const double4 z = step(S, ts, row.s, lr.v, i, CoefPtr{ctile + c, cstr}, ai, Ui, lai);
       const double4 vm = F.epi_vm1 ? ldv(F.epi_vm1 + i) : d4(0.0);
       epi(i, z, ai, vm);
     }
