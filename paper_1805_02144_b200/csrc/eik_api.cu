@@ -1403,6 +1403,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   int e1max = 1, e2max = 1;
   {
     std::vector<int32_t> loc(N, -1), list;
+    bool sort_halo = false;
+    if (const char* e = getenv("EIK_SORT_HALO")) sort_halo = atoi(e) != 0;
     for (int t = 0; t < NT; ++t) {
       const int64_t lo = tstart[t], hi = tstart[t + 1];
       list.clear();
@@ -1422,6 +1424,13 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
         }
       }
       const int nE2 = (int)list.size();
+      if (sort_halo) {
+        // each halo ring in ascending device order (labels only: the stencil
+        // sums keep their slot order)
+        std::sort(list.begin() + nT, list.begin() + nE1);
+        std::sort(list.begin() + nE1, list.end());
+        for (int c2 = nT; c2 < nE2; ++c2) loc[list[c2]] = c2;
+      }
       if (nE2 > 32767) return fail(EIK_EINVAL, "tile halo too large");
       t_cell0[t] = (int32_t)lo; t_nT[t] = nT; t_nE1[t] = nE1; t_nE2[t] = nE2;
       t_e2off[t] = (int32_t)e2map.size();
