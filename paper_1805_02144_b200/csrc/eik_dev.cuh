@@ -2101,7 +2101,7 @@ __device__ void eng_finish_attempt(cg::grid_group& grid, Smem& sm, const Op& op,
                                    const EngineTask& T, const EngineWork& Wk, ES& E,
                                    bool dense_ready = false) {
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  const int64_t NU = Wk.NU, n = Wk.n, ld = Wk.m_alloc;
+  const int64_t NU = Wk.NU, n = Wk.n;
   int64_t lo, hi;
   brange(NU, lo, hi);
   ProfClock pc;
