@@ -508,6 +508,10 @@ struct JvAcc {
 #define EIK_CANDU 4
 #endif
 constexpr int kCandU = EIK_CANDU;
+// EIK_SHDIV: form_x divides by h through a shared reciprocal (see there)
+#ifndef EIK_SHDIV
+#define EIK_SHDIV 1
+#endif
 // EIK_ROW0: every thread loads row threadIdx.x of the tile's step-2 rows
 // before the barrier that ends step 1 and keeps it for step 3 (own cells)
 #ifndef EIK_ROW0
@@ -863,7 +867,22 @@ __device__ __forceinline__ double4 form_x(const Form& f, double4 s0, double4 s1,
   double4 x = s0;
   if (f.vm2) x = x - f.a1 * s1;
   if (f.vm1) x = x - f.a2 * s2;
+#if EIK_SHDIV
+  // x / h for the four components with one shared reciprocal (the tiled pass
+  // forms two halo cells per thread: 8 divisions by the same h): r = RN(1 / h),
+  // q0 = RN(x r), q = RN(q0 + (x - q0 h) r) with the remainder exact by FMA --
+  // the correctly rounded quotient (Markstein), i.e. the same bits as x / h
+  // unless h's significand is all ones (tests/host/shared_div.c compares the
+  // two on 2e7 random pairs)
+  const double r = 1.0 / f.h;
+  auto dv = [&](double a) {
+    const double q0 = a * r;
+    return fma(fma(-q0, f.h, a), r, q0);
+  };
+  return make_double4(dv(x.x), dv(x.y), dv(x.z), dv(x.w));
+#else
   return div4(x, f.h);
+#endif
 }
 
 // this CTA's tiles are t = blockIdx.x + k * gridDim.x, k < tile_count; rev walks

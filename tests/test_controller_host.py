@@ -94,3 +94,13 @@ def test_pow_over_factorial(ctl):
     for t in (0.0, 0.37, 0.5, 0.9, 1.0):
         for ell in range(6):
             assert ctl.t_powfact(t, ell) == t ** ell / math.factorial(ell)
+
+
+def test_shared_reciprocal_division_is_exact(tmp_path):
+    """form_x's x / h through one shared reciprocal and two FMAs (the tiled
+    pass, csrc/eik_dev.cuh) gives the bits of IEEE division."""
+    exe = tmp_path / "shared_div"
+    subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off", "-o", str(exe),
+                    os.path.join(HERE, "host", "shared_div.c"), "-lm"], check=True)
+    out = subprocess.run([str(exe), "20000000"], check=True, capture_output=True, text=True)
+    assert int(out.stdout.strip()) == 0
