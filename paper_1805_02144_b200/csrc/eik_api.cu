@@ -1498,22 +1498,24 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
   // tile-major coefficient blocks: each tile's 54 runs contiguous (run stride
   // nT rounded up to 16 doubles, so every run starts on a 128-byte line) instead
   // of 54 global runs of N: a tile streams one ~100 KB block, not 54 2-KB pieces
-  // 5 MB apart.  EIK_TILECOEF=0 (environment) keeps the global runs.
+  // 5 MB apart.  With EIK_FIXCS (default) the run stride is TILE for every tile.
   bool tilecoef = !EIK_LPT;
-  if (const char* e = getenv("EIK_TILECOEF")) tilecoef = tilecoef && atoi(e) != 0;
+  if (!EIK_FIXCS)
+    if (const char* e = getenv("EIK_TILECOEF")) tilecoef = tilecoef && atoi(e) != 0;
   std::vector<int32_t> t_coff(NTb, 0);
   if (tilecoef) {
     size_t tot = 0;
     for (int t = 0; t < NTb; ++t) {
       t_coff[t] = (int32_t)(tot / 16);
-      tot += (size_t)NCOEF * ((t_nT[t] + 15) & ~15);
+      tot += (size_t)NCOEF * (EIK_FIXCS ? TILE : ((t_nT[t] + 15) & ~15));
     }
     if (tot / 16 > (size_t)INT32_MAX) {
       tilecoef = false;
     } else {
       std::vector<double> blk(tot + 16, 0.0);
       for (int t = 0; t < NTb; ++t) {
-        const size_t cs = (size_t)((t_nT[t] + 15) & ~15), b0 = (size_t)t_coff[t] * 16;
+        const size_t cs = EIK_FIXCS ? (size_t)TILE : (size_t)((t_nT[t] + 15) & ~15);
+        const size_t b0 = (size_t)t_coff[t] * 16;
         for (int r = 0; r < NCOEF; ++r)
           for (int cc = 0; cc < t_nT[t]; ++cc)
             blk[b0 + r * cs + cc] = coefc[(size_t)r * NC + t_cell0[t] + cc];
@@ -1522,6 +1524,8 @@ eik_status eik_swe_create(int32_t n_g, const EikCsrView* ops, const double* n_x,
     }
     if (!tilecoef) std::fill(t_coff.begin(), t_coff.end(), 0);
   }
+  if (EIK_FIXCS && !tilecoef)
+    return fail(EIK_EINVAL, "the fixed-stride build needs the tile-major coefficient blocks");
   EikSwe* c = new EikSwe();
   c->N = N;
   c->K = K;

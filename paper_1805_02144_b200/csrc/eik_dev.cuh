@@ -270,8 +270,9 @@ struct SweOp {
   const int* e2map;      // local -> global cell id, order [own, H1, H2]
   const short* lnbr;     // [rows][8] local off-diagonal neighbours of E1 cells
   const double* coefc;   // off-diagonal G, D, V (compact stencil), 54 runs (slot-major) per
-                         // tile: tile-major blocks [tile][54][pad16(nT)] at t_coff * 16
-                         // (tilecoef), or global runs [54][NC]
+                         // tile: tile-major blocks [tile][54][TILE] at t_coff * 16
+                         // (tilecoef; run stride pad16(nT) without EIK_FIXCS), or the
+                         // global runs [54][NC]
   int64_t NC;            // global run stride (N rounded up to even)
   const int* t_coff;     // per tile: block offset / 16 doubles (0 for global runs)
   int tilecoef;
@@ -542,10 +543,25 @@ struct CoefChunk {
   double v[CH][9];
 };
 // cptr: the cell's entry of run 0, cs: run stride (doubles)
+// EIK_FIXCS (default): every tile block has run stride TILE, so the 54 loads
+// of a cell are one base register plus immediate offsets (no per-load address
+// arithmetic); 0 keeps the run stride a run-time value (pad16(nT) blocks, or
+// the global runs with EIK_TILECOEF=0 in the environment)
+#ifndef EIK_FIXCS
+#define EIK_FIXCS 1
+#endif
+#if EIK_FIXCS
+struct CoefPtr {
+  const double* p;
+  static constexpr int64_t cs = TPB;
+  __device__ __forceinline__ CoefPtr(const double* q, int64_t) : p(q) {}
+};
+#else
 struct CoefPtr {
   const double* p;
   int64_t cs;
 };
+#endif
 template <int CH>
 __device__ __forceinline__ void coef_load(const CoefPtr& C, int s0, CoefChunk<CH>& cf) {
   const int64_t st = (int64_t)9 * C.cs;
@@ -973,7 +989,11 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     const double* lce1 = S.LcE1 + (int64_t)e1off * 6;
     // the tile's 54 coefficient runs: entry of own cell c at ctile + c, run stride cstr
     const double* ctile = S.tilecoef ? S.coefc + (int64_t)cur.coff * 16 : S.coefc + c0;
+#if EIK_FIXCS
+    constexpr int64_t cstr = TPB;
+#else
     const int64_t cstr = S.tilecoef ? (int64_t)((nT + 15) & ~15) : S.NC;
+#endif
     if (EIK_PF2 && !Step::kE1Only) {
       // step-2 rows of this tile: nE1 x 16 B (rows) + nE1 x 48 B (Laplacian)
       const int l1 = (nE1 * 16 + 127) >> 7, l2 = (nE1 * 48 + 127) >> 7;

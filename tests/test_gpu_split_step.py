@@ -44,7 +44,7 @@ print(json.dumps(out))
 
 def _run(mono, host=False, extra=None):
     env = dict(os.environ)
-    for k in ("EIK_STEP_MONO", "EIK_STEP_HOST", "EIK_TILECOEF", "EIK_SORT_HALO",
+    for k in ("EIK_STEP_MONO", "EIK_STEP_HOST", "EIK_SORT_HALO",
               "EIK_TILES_EXTRA"):
         env.pop(k, None)
     env.update(extra or {})
@@ -84,11 +84,10 @@ def test_hostloop_matches_graph_bitwise():
 
 def test_layout_knobs_do_not_change_results():
     """The device layout choices made at context creation are labels only:
-    global coefficient runs instead of the tile-major blocks (EIK_TILECOEF=0)
-    and halo rings sorted by device index (EIK_SORT_HALO=1) give the same bits
-    and counters as the default layout."""
+    halo rings sorted by device index (EIK_SORT_HALO=1) give the same bits and
+    counters as the default layout."""
     base = _run(False)
-    for extra in ({"EIK_TILECOEF": "0"}, {"EIK_SORT_HALO": "1"}):
+    for extra in ({"EIK_SORT_HALO": "1"},):
         other = _run(False, extra=extra)
         for k in base:
             assert base[k]["calls"] == other[k]["calls"], (extra, k)
