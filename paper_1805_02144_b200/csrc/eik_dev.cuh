@@ -997,9 +997,14 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     if (EIK_PF2 && !Step::kE1Only) {
       // step-2 rows of this tile: nE1 x 16 B (rows) + nE1 x 48 B (Laplacian)
       const int l1 = (nE1 * 16 + 127) >> 7, l2 = (nE1 * 48 + 127) >> 7;
-      for (int q = threadIdx.x; q < l1 + l2; q += TPB)
+      auto pf = [&](int q) {
         prefetch_l1(q < l1 ? (const char*)rows + ((int64_t)q << 7)
                            : (const char*)lce1 + ((int64_t)(q - l1) << 7));
+      };
+      // one line per thread covers a tile of up to TPB cells (no loop in the common case)
+      if ((int)threadIdx.x < l1 + l2) pf(threadIdx.x);
+      if (l1 + l2 > TPB)
+        for (int q = threadIdx.x + TPB; q < l1 + l2; q += TPB) pf(q);
     }
     // step 1: x on E2 (two cells per thread per round, all loads issued first)
     const int nEs = Step::kE1Only ? nE1 : nE2;  // cells staged in step 1
@@ -1060,7 +1065,9 @@ __device__ void swe_tiled_op(Smem& sm, const SweOp& S, const Form& F, const Step
     if (EIK_PF4) {
       const int ln = (nT * 32 + 127) >> 7;
       const int nv = F.epi_vm1 ? 2 * ln : ln;
-      for (int q = threadIdx.x; q < nv; q += TPB)
+      // nv <= 2 * ceil(TPB * 32 / 128) <= TPB lines: one predicated prefetch per thread
+      const int q = threadIdx.x;
+      if (q < nv)
         prefetch_l1(q < ln ? (const char*)(S.ne + c0) + ((int64_t)q << 7)
                            : (const char*)(F.epi_vm1 + c0) + ((int64_t)(q - ln) << 7));
     }
